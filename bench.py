@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: points hashed + indexed per second.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--scheme CS_E2LSH]
+    python bench.py --impl reference ...      # the oracle on host cores (reference arm)
+
+A step = one pass of the whole hot path over the config's synthetic batch:
+hash every point (sketch -> discretise -> keys, §8(a) a-2..a-4), group the points
+into the buckets of all L tables (a-5), at N > 1 the NCCL all-gather of the
+per-table coarse bucket counts (a-6), and a bucket lookup for a query batch
+(a-7).  Points are sharded across ranks (C4: n = 1e6 total, strong scaling).
+Inputs are resident in HBM when the timed region starts; `e2e` times the same
+step through the C ABI from pinned HOST buffers (H2D of X and the queries, D2H
+of the per-table bucket counts and query ranges inside the timed region).
+Rank 0 prints one JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "points hashed+indexed/sec"
+UNIT = "points/s"
+NQ = 1000          # queries looked up per step (a-7)
+B_COARSE = 12      # coarse bins exchanged across ranks (§8(e))
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--scheme", default="CS_E2LSH")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
+        int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def shard(n, rank, world):
+    per = (n + world - 1) // world
+    lo = min(n, rank * per)
+    return lo, min(n, lo + per)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(config, scheme):
+    """dram bytes per launch of the sketch kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            js = json.load(f)
+        ent = js.get(f"{config}/{scheme}/sketch")
+        return ent.get("dram_bytes_per_launch") if ent else None
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------------------
+# reference arm: the oracle on host cores
+# --------------------------------------------------------------------------
+
+def oracle_step_sample(cfg, scheme, rows):
+    import numpy as np
+    from oracle import lsh
+    import synth
+    kw = dict(mode_d=cfg.mode_d, mode_m=cfg.mode_m) if scheme.startswith("HCS") else {}
+    p = lsh.Params(scheme, d=cfg.d, m=cfg.m, L=cfg.L, K=cfg.K, w=cfg.w, seed=cfg.hash_seed, **kw)
+    X = synth.rows(cfg, 0, rows).numpy()
+    t0 = time.perf_counter()
+    t = lsh.make_tables(p) if not hasattr(oracle_step_sample, "_t") else oracle_step_sample._t
+    oracle_step_sample._t = t
+    out = lsh.hash_points(p, t, X)
+    lsh.group(out["keys"])
+    return time.perf_counter() - t0
+
+
+def cpu_sample_rows(cfg):
+    # ~10-30 s of single-core NumPy work for the bounded sample
+    return {"C1": cfg.n, "C2": 20000, "C3": 4000, "C4": 20000, "C5": 200}.get(cfg.name, 2000)
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import synth
+    cfg = synth.CONFIGS[args.config]
+    rows = min(cfg.n, cpu_sample_rows(cfg))
+    times = []
+    for i in range(args.warmup + args.steps):
+        dt = oracle_step_sample(cfg, args.scheme, rows)
+        if i >= args.warmup:
+            times.append(dt)
+    tstep = statistics.median(times)
+    value = rows / tstep
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tstep * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}:{args.scheme}", "n": cfg.n, "d": cfg.d, "m": cfg.m, "L": cfg.L,
+                       "K": cfg.K, "w": cfg.w, "sample_rows_per_step": rows},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"first {rows} rows of {cfg.name} per step (hash + group), NumPy fp64"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    import numpy as np
+    import paper_2503_06737_b200 as pk
+    import synth
+
+    cfg = synth.CONFIGS[args.config]
+    scheme = args.scheme
+    kw = dict(mode_d=cfg.mode_d, mode_m=cfg.mode_m) if scheme.startswith("HCS") else {}
+    h = pk.LSH(scheme, cfg.d, cfg.m, cfg.L, cfg.K, cfg.w, cfg.hash_seed, device=dev.index, **kw)
+    lo, hi = shard(cfg.n, rank, world)
+    n_local = hi - lo
+    X = synth.rows(cfg, lo, hi, device=dev)
+    Q = synth.rows(cfg, 0, NQ, device=dev) if rank == 0 else synth.rows(cfg, lo, lo + min(NQ, n_local), device=dev)
+    nq = Q.shape[0]
+    stream = torch.cuda.current_stream()
+    counts_all = torch.empty((world, cfg.L, 1 << B_COARSE), dtype=torch.int32, device=dev)
+    begin = torch.empty((nq, cfg.L), dtype=torch.int64, device=dev)
+    end = torch.empty((nq, cfg.L), dtype=torch.int64, device=dev)
+
+    def step():
+        idx = h.build_index(X, id_base=lo)
+        if world > 1:
+            cnt = idx.counts(B_COARSE)
+            dist.all_gather_into_tensor(counts_all, cnt.unsqueeze(0))
+        b, e = h.query_buckets(idx, Q)
+        return idx, b, e
+
+    # warm-up
+    for _ in range(max(3, args.warmup)):
+        idx, _, _ = step()
+    torch.cuda.synchronize()
+    del idx
+
+    # device-timed region (inputs resident in HBM; X >> L2 so no flush needed)
+    pk.timing_reset()
+    pk.timing_enable(True)
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = pk.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    keep = []
+    ev0.record(stream)
+    for _ in range(args.steps):
+        keep.append(step()[0])
+        if len(keep) > 2:
+            keep.pop(0)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = pk.launch_count() - l0
+    clk = clocks.stop()
+    pk.timing_enable(False)
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    sketch_ms, sketch_n = pk.timing_get("sketch")
+    kernel_ms = {k: pk.timing_get(k)[0] / max(1, args.steps) for k in
+                 ("sketch", "radix_upsweep", "radix_scan", "radix_downsweep", "segsort", "rle", "lookup", "counts",
+                  "dense_gemm", "keys_from_proj")}
+    keep.clear()
+    t = torch.tensor([ms_local], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = cfg.n / (ms * 1e-3)
+
+    # end-to-end through the C ABI from pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        Xh = X.cpu().pin_memory()
+        Qh = Q.cpu().pin_memory()
+        Xd = torch.empty_like(X)
+        Qd = torch.empty_like(Q)
+        nb_h = torch.empty((cfg.L, 1 << B_COARSE), dtype=torch.int32).pin_memory()
+        be_h = torch.empty((2, nq, cfg.L), dtype=torch.int64).pin_memory()
+
+        def e2e_step():
+            Xd.copy_(Xh, non_blocking=True)
+            Qd.copy_(Qh, non_blocking=True)
+            idx = h.build_index(Xd, id_base=lo)
+            cnt = idx.counts(B_COARSE)
+            if world > 1:
+                dist.all_gather_into_tensor(counts_all, cnt.unsqueeze(0))
+            b, e = h.query_buckets(idx, Qd)
+            nb_h.copy_(cnt, non_blocking=True)
+            be_h[0].copy_(b, non_blocking=True)
+            be_h[1].copy_(e, non_blocking=True)
+            return idx
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        esteps = max(2, min(args.steps, 5))
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(esteps):
+            ix = e2e_step()
+        a1.record(stream)
+        torch.cuda.synchronize()
+        del ix
+        te = torch.tensor([a0.elapsed_time(a1) / esteps], device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": cfg.n / (float(te.item()) * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(X.numel() * 4 + Q.numel() * 4),
+               "d2h_bytes_per_step": int(nb_h.numel() * 4 + be_h.numel() * 8)}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    hbm_peak, peak_kind = peaks()
+    bytes_per_point = 4 * cfg.d + 8 * cfg.L          # sketch kernel: read the point, write its L keys
+    sketch_avg_ms = sketch_ms / max(1, sketch_n)
+    achieved = bytes_per_point * n_local / (sketch_avg_ms * 1e-3) / 1e9 if sketch_avg_ms > 0 else None
+    traffic = ncu_traffic(cfg.name, scheme)
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        rows = min(cfg.n, cpu_sample_rows(cfg))
+        oracle_step_sample(cfg, scheme, min(rows, 256))  # warm caches / table draw
+        dt = oracle_step_sample(cfg, scheme, rows)
+        cpu = {"value": rows / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"first {rows} rows of {cfg.name}, hash + group, NumPy fp64 (single-threaded)"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}:{scheme}", "n": cfg.n, "d": cfg.d, "m": cfg.m, "L": cfg.L,
+                   "K": cfg.K, "w": cfg.w, "queries_per_step": NQ, "parallelism": f"points sharded x{world}",
+                   "l2": "inputs (%.2f GB) larger than L2; no flush" % (cfg.n * cfg.d * 4 / 1e9)},
+        "roofline": {"kernel": "sketch", "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
+                     "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": (achieved / hbm_peak) if achieved else None,
+                     "bytes_per_point": bytes_per_point, "traffic": traffic,
+                     "avg_launch_ms": sketch_avg_ms},
+        "kernel_ms_per_step": kernel_ms,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -233,13 +233,25 @@ def fingerprint(words: Sequence[int]) -> int:
     return rng.fmix64(f)
 
 
+def _fmix64_np(z: np.ndarray) -> np.ndarray:
+    """rng.fmix64 applied elementwise (numpy uint64 arithmetic wraps mod 2^64)."""
+    z = z.astype(np.uint64)
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
 def e2lsh_keys(codes: np.ndarray, L: int, K: int) -> np.ndarray:
+    """fingerprint() of every (point, table), elementwise over points (uint64 [L][n])."""
     n = codes.shape[0]
     out = np.zeros((L, n), dtype=np.uint64)
-    for t in range(L):
-        block = codes[:, t * K:(t + 1) * K]
-        for i in range(n):
-            out[t, i] = fingerprint(block[i].tolist())
+    words = (np.asarray(codes, dtype=np.int64) & 0xFFFFFFFF).astype(np.uint64)
+    with np.errstate(over="ignore"):
+        for t in range(L):
+            f = np.full(n, rng.FNV64_OFFSET, dtype=np.uint64)
+            for k in range(K):
+                f = (f ^ words[:, t * K + k]) * np.uint64(rng.FNV64_PRIME)
+            out[t] = _fmix64_np(f)
     return out
 
 

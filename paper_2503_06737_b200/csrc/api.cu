@@ -1,0 +1,704 @@
+// api.cu — host core of the C ABI declared in include/lsh.h.
+//
+// Validates the problem statement, draws the random parameters on the host
+// (params.hpp, R1-R4), plans the device execution (per-chunk bin lists
+// for the sketch kernel), owns device buffers of handles and indexes, and
+// launches the kernels of sketch.cu / dense.cu / group.cu on the caller's stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/lsh.h"
+#include "internal.hpp"
+#include "params.hpp"
+
+using namespace lshb;
+
+// ---------------------------------------------------------------------------
+// errors, launch counting, timing
+// ---------------------------------------------------------------------------
+static std::mutex g_err_mu;
+static std::string g_last_cuda_error = "";
+static std::atomic<uint64_t> g_launches{0};
+
+static lsh_status cuda_fail(cudaError_t e, const char* where) {
+    std::lock_guard<std::mutex> g(g_err_mu);
+    g_last_cuda_error = std::string(where) + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? LSH_ENOMEM : LSH_ECUDA;
+}
+#define CK(call)                                              \
+    do {                                                      \
+        cudaError_t e_ = (call);                              \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call);   \
+    } while (0)
+
+namespace lshb {
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+struct TimingSlot {
+    double ms = 0;
+    int64_t launches = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+    cudaEvent_t open = nullptr;
+};
+static std::mutex g_time_mu;
+static std::atomic<int> g_timing_on{0};
+static std::map<std::string, TimingSlot> g_slots;
+static std::vector<cudaEvent_t> g_event_pool;
+
+static cudaEvent_t get_event() {
+    if (!g_event_pool.empty()) {
+        cudaEvent_t e = g_event_pool.back();
+        g_event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+void timing_begin(const char* name, cudaStream_t s) {
+    if (!g_timing_on.load()) return;
+    std::lock_guard<std::mutex> g(g_time_mu);
+    TimingSlot& sl = g_slots[name];
+    sl.open = get_event();
+    cudaEventRecord(sl.open, s);
+}
+void timing_end(const char* name, cudaStream_t s) {
+    if (!g_timing_on.load()) return;
+    std::lock_guard<std::mutex> g(g_time_mu);
+    TimingSlot& sl = g_slots[name];
+    if (!sl.open) return;
+    cudaEvent_t e = get_event();
+    cudaEventRecord(e, s);
+    sl.pending.emplace_back(sl.open, e);
+    sl.open = nullptr;
+    sl.launches++;
+}
+}  // namespace lshb
+
+extern "C" uint64_t lsh_launch_count(void) { return g_launches.load(); }
+extern "C" void lsh_timing_enable(int32_t on) { g_timing_on.store(on ? 1 : 0); }
+extern "C" void lsh_timing_reset(void) {
+    std::lock_guard<std::mutex> g(g_time_mu);
+    for (auto& kv : g_slots) {
+        for (auto& pr : kv.second.pending) {
+            g_event_pool.push_back(pr.first);
+            g_event_pool.push_back(pr.second);
+        }
+        kv.second = TimingSlot();
+    }
+}
+extern "C" lsh_status lsh_timing_get(const char* name, double* ms, int64_t* launches) {
+    CK(cudaDeviceSynchronize());
+    std::lock_guard<std::mutex> g(g_time_mu);
+    auto it = g_slots.find(name);
+    if (it == g_slots.end()) {
+        if (ms) *ms = 0;
+        if (launches) *launches = 0;
+        return LSH_OK;
+    }
+    TimingSlot& sl = it->second;
+    for (auto& pr : sl.pending) {
+        float t = 0;
+        cudaEventElapsedTime(&t, pr.first, pr.second);
+        sl.ms += t;
+        g_event_pool.push_back(pr.first);
+        g_event_pool.push_back(pr.second);
+    }
+    sl.pending.clear();
+    if (ms) *ms = sl.ms;
+    if (launches) *launches = sl.launches;
+    return LSH_OK;
+}
+
+extern "C" const char* lsh_last_cuda_error(void) {
+    static thread_local std::string copy;
+    std::lock_guard<std::mutex> g(g_err_mu);
+    copy = g_last_cuda_error;
+    return copy.c_str();
+}
+
+extern "C" const char* lsh_strerror(lsh_status s) {
+    switch (s) {
+        case LSH_OK: return "ok";
+        case LSH_EINVAL: return "invalid parameters";
+        case LSH_EDIM: return "invalid dimension or size";
+        case LSH_ENOMEM: return "out of device memory";
+        case LSH_ECUDA: return "CUDA error";
+        case LSH_EOVERFLOW: return "E2LSH code outside int32";
+        case LSH_ESTATE: return "invalid handle or state";
+        case LSH_EUNSUPPORTED: return "unsupported shape for this build";
+    }
+    return "unknown status";
+}
+
+// ---------------------------------------------------------------------------
+// parameter validation and the host-side draw
+// ---------------------------------------------------------------------------
+static bool is_dense(int s) { return s == LSH_E2LSH || s == LSH_SRP; }
+static bool is_hcs(int s) { return s == LSH_HCS_E2LSH || s == LSH_HCS_SRP; }
+static bool is_e2lsh(int s) { return s == LSH_E2LSH || s == LSH_CS_E2LSH || s == LSH_HCS_E2LSH; }
+
+static lsh_status validate(const lsh_params* p) {
+    if (!p) return LSH_ESTATE;
+    if (p->scheme < 0 || p->scheme > 5) return LSH_EINVAL;
+    if (p->d < 1 || p->d > (1ll << 27)) return LSH_EINVAL;
+    if (p->m < 1 || p->m > (1 << 20) || p->L < 1 || p->K < 1) return LSH_EINVAL;
+    if ((int64_t)p->L * p->K != p->m) return LSH_EINVAL;
+    if (!(p->w > 0.0f) || !std::isfinite(p->w)) return LSH_EINVAL;
+    if (!is_e2lsh(p->scheme) && p->K > 64) return LSH_EINVAL;
+    if (p->reserved != 0) return LSH_EINVAL;
+    if (is_hcs(p->scheme)) {
+        if (p->N < 1 || p->N > LSH_MAX_MODES) return LSH_EINVAL;
+        int64_t pd = 1, pm = 1;
+        for (int k = 0; k < p->N; ++k) {
+            if (p->mode_d[k] < 1 || p->mode_m[k] < 1) return LSH_EINVAL;
+            pd *= p->mode_d[k];
+            pm *= p->mode_m[k];
+            if (pd > (1ll << 40)) return LSH_EINVAL;
+        }
+        if (pm != p->m || pd < p->d) return LSH_EINVAL;
+    } else {
+        if (p->N != 1) return LSH_EINVAL;
+    }
+    return LSH_OK;
+}
+
+struct HostTables {
+    int N = 1;
+    std::vector<int64_t> md, mm;             // mode sizes
+    std::vector<std::vector<int32_t>> h, s;  // per mode
+    std::vector<TwoWise> fb, fs;             // per mode families
+    std::vector<float> b;
+    std::vector<uint16_t> R;                 // dense only, bf16 bits [m][d]
+};
+
+static void draw(const lsh_params* p, HostTables& t, bool with_gaussian) {
+    offsets(p->seed, p->m, p->w, t.b);
+    if (is_dense(p->scheme)) {
+        t.N = 1;
+        if (with_gaussian) {
+            const int64_t total = (int64_t)p->m * p->d;
+            t.R.assign(total, 0);
+            const int64_t pairs = (total + 1) / 2;
+            unsigned nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+            if (pairs < 65536) nth = 1;
+            std::vector<std::thread> th;
+            for (unsigned k = 0; k < nth; ++k) {
+                const int64_t lo = pairs * k / nth, hi = pairs * (k + 1) / nth;
+                th.emplace_back([&, lo, hi]() { gaussian_range(p->seed, total, lo, hi, t.R.data()); });
+            }
+            for (auto& x : th) x.join();
+        }
+        return;
+    }
+    t.N = is_hcs(p->scheme) ? p->N : 1;
+    for (int k = 0; k < t.N; ++k) {
+        const int64_t dk = is_hcs(p->scheme) ? p->mode_d[k] : p->d;
+        const int64_t mk = is_hcs(p->scheme) ? p->mode_m[k] : p->m;
+        t.md.push_back(dk);
+        t.mm.push_back(mk);
+        TwoWise fb = bucket_family(p->seed, k, (uint64_t)mk);
+        TwoWise fs = sign_family(p->seed, k);
+        t.fb.push_back(fb);
+        t.fs.push_back(fs);
+        std::vector<int32_t> hv(dk), sv(dk);
+        for (int64_t i = 0; i < dk; ++i) {
+            hv[i] = (int32_t)fb.eval((uint64_t)i);
+            sv[i] = fs.eval((uint64_t)i) == 0 ? 1 : -1;
+        }
+        t.h.push_back(std::move(hv));
+        t.s.push_back(std::move(sv));
+    }
+}
+
+// Per input coordinate j < d: the bin it adds to and its sign (Def. CS: h(j), s(j);
+// Def. HCS: l = sum_k h_k(i_k) prod_{t<k} m_t, sign = prod_k s_k(i_k) with
+// (i_1..i_N) the column-major unflatten of j).
+static void coordinate_map(const lsh_params* p, const HostTables& t, std::vector<int32_t>& bin,
+                           std::vector<int8_t>& sgn) {
+    bin.resize(p->d);
+    sgn.resize(p->d);
+    for (int64_t j = 0; j < p->d; ++j) {
+        int64_t rem = j, l = 0, stride = 1;
+        int sg = 1;
+        for (int k = 0; k < t.N; ++k) {
+            const int64_t ik = rem % t.md[k];
+            rem /= t.md[k];
+            l += (int64_t)t.h[k][ik] * stride;
+            stride *= t.mm[k];
+            sg *= t.s[k][ik];
+        }
+        bin[j] = (int32_t)l;
+        sgn[j] = (int8_t)sg;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// handle
+// ---------------------------------------------------------------------------
+struct lsh_handle {
+    lsh_params p{};
+    HostTables host;
+    int device = 0, num_sms = 148;
+    int key_width = 64;
+    SketchPlanDev plan{};
+    DiscretizeDev disc{};
+    uint32_t* d_entries = nullptr;
+    int32_t* d_binptr = nullptr;
+    float* d_coff = nullptr;
+    uint16_t* d_R = nullptr;
+    int* d_flags = nullptr;
+    std::vector<int32_t*> d_h, d_s;
+    float* d_b = nullptr;
+    bool sketch_ok = true;
+};
+
+struct lsh_index {
+    const lsh_handle* h = nullptr;
+    int64_t n = 0;
+    int L = 0;
+    IndexDev dev{};
+    void* mem = nullptr;
+    uint32_t* nb_host = nullptr;
+    cudaEvent_t done = nullptr;
+    cudaStream_t stream = nullptr;  // build stream: memory is freed stream-ordered on it
+};
+
+static lsh_status build_plan(lsh_handle* H) {
+    const lsh_params* p = &H->p;
+    std::vector<int32_t> bin;
+    std::vector<int8_t> sgn;
+    coordinate_map(p, H->host, bin, sgn);
+    const int d = (int)p->d, m = p->m;
+    int vpt = 0;
+    for (int v : {1, 2, 4, 8, 16})
+        if (64 * v >= d) {
+            vpt = v;
+            break;
+        }
+    int nchunks = 1;
+    if (!vpt) {
+        // chunked: partial bins of the tile live in shared memory
+        vpt = 16;
+        if (sketch_smem_bytes(64 * vpt, m, 2) > 232448) vpt = 8;
+        nchunks = (d + 64 * vpt - 1) / (64 * vpt);
+        if (sketch_smem_bytes(64 * vpt, m, nchunks) > 232448) {
+            H->sketch_ok = false;
+            return LSH_OK;
+        }
+    }
+    const int Q = 64 * vpt;
+    std::vector<int32_t> bin_ptr((size_t)nchunks * (m + 1), 0);
+    std::vector<uint32_t> entries(d);
+    for (int c = 0; c < nchunks; ++c) {
+        const int j0 = c * Q, j1 = std::min(d, (c + 1) * Q);
+        int32_t* bp = bin_ptr.data() + (size_t)c * (m + 1);
+        std::vector<int32_t> cnt(m + 1, 0);
+        for (int j = j0; j < j1; ++j) cnt[bin[j] + 1]++;
+        for (int l = 0; l < m; ++l) cnt[l + 1] += cnt[l];
+        for (int l = 0; l <= m; ++l) bp[l] = j0 + cnt[l];
+        std::vector<int32_t> cur(cnt.begin(), cnt.end() - 1);
+        for (int j = j0; j < j1; ++j) {  // ascending j inside each bin
+            const int k = j - j0;
+            const uint32_t off = (uint32_t)((k >> 2) * 129 + (k & 3) * 32);
+            entries[j0 + cur[bin[j]]++] = off | (sgn[j] < 0 ? 0x80000000u : 0u);
+        }
+    }
+    CK(cudaMalloc(&H->d_entries, sizeof(uint32_t) * std::max(1, d)));
+    CK(cudaMalloc(&H->d_binptr, sizeof(int32_t) * bin_ptr.size()));
+    CK(cudaMemcpy(H->d_entries, entries.data(), sizeof(uint32_t) * d, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(H->d_binptr, bin_ptr.data(), sizeof(int32_t) * bin_ptr.size(), cudaMemcpyHostToDevice));
+    H->plan = SketchPlanDev{d, m, p->L, p->K, Q, vpt, nchunks, H->d_entries, H->d_binptr};
+    return LSH_OK;
+}
+
+static void free_handle(lsh_handle* H) {
+    if (!H) return;
+    cudaFree(H->d_entries);
+    cudaFree(H->d_binptr);
+    cudaFree(H->d_coff);
+    cudaFree(H->d_R);
+    cudaFree(H->d_flags);
+    for (auto x : H->d_h) cudaFree(x);
+    for (auto x : H->d_s) cudaFree(x);
+    cudaFree(H->d_b);
+    delete H;
+}
+
+extern "C" lsh_status lsh_create(const lsh_params* p, lsh_handle** out) {
+    if (!out) return LSH_ESTATE;
+    *out = nullptr;
+    lsh_status st = validate(p);
+    if (st != LSH_OK) return st;
+    lsh_handle* H = new lsh_handle();
+    H->p = *p;
+    H->device = p->device;
+    auto fail = [&](lsh_status s) {
+        free_handle(H);
+        return s;
+    };
+    cudaError_t e = cudaSetDevice(p->device);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaSetDevice"));
+    cudaDeviceGetAttribute(&H->num_sms, cudaDevAttrMultiProcessorCount, p->device);
+    draw(p, H->host, true);
+    H->key_width = is_e2lsh(p->scheme) ? 64 : p->K;
+    const int m = p->m;
+    // offsets folded with w: c_off[l] = b_l / w; c_scale = sqrt(m)/w (CS/HCS) or 1/w (dense)
+    std::vector<float> coff(m);
+    for (int l = 0; l < m; ++l) coff[l] = (float)((double)H->host.b[l] / (double)p->w);
+    const double scale = is_dense(p->scheme) ? 1.0 : (double)sqrtf((float)m);
+    H->disc.e2lsh = is_e2lsh(p->scheme) ? 1 : 0;
+    H->disc.c_scale = (float)(scale / (double)p->w);
+    if ((e = cudaMalloc(&H->d_coff, sizeof(float) * m)) != cudaSuccess) return fail(cuda_fail(e, "malloc"));
+    if ((e = cudaMemcpy(H->d_coff, coff.data(), sizeof(float) * m, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return fail(cuda_fail(e, "memcpy"));
+    if ((e = cudaMalloc(&H->d_flags, sizeof(int))) != cudaSuccess) return fail(cuda_fail(e, "malloc"));
+    cudaMemset(H->d_flags, 0, sizeof(int));
+    H->disc.c_off = H->d_coff;
+    H->disc.flags = H->d_flags;
+    if ((e = cudaMalloc(&H->d_b, sizeof(float) * m)) != cudaSuccess) return fail(cuda_fail(e, "malloc"));
+    cudaMemcpy(H->d_b, H->host.b.data(), sizeof(float) * m, cudaMemcpyHostToDevice);
+    if (is_dense(p->scheme)) {
+        const size_t bytes = sizeof(uint16_t) * H->host.R.size();
+        if ((e = cudaMalloc(&H->d_R, bytes)) != cudaSuccess) return fail(cuda_fail(e, "malloc R"));
+        if ((e = cudaMemcpy(H->d_R, H->host.R.data(), bytes, cudaMemcpyHostToDevice)) != cudaSuccess)
+            return fail(cuda_fail(e, "memcpy R"));
+    } else {
+        for (int k = 0; k < H->host.N; ++k) {
+            int32_t *dh = nullptr, *ds = nullptr;
+            const size_t bytes = sizeof(int32_t) * H->host.h[k].size();
+            if ((e = cudaMalloc(&dh, bytes)) != cudaSuccess) return fail(cuda_fail(e, "malloc h"));
+            H->d_h.push_back(dh);
+            if ((e = cudaMalloc(&ds, bytes)) != cudaSuccess) return fail(cuda_fail(e, "malloc s"));
+            H->d_s.push_back(ds);
+            cudaMemcpy(dh, H->host.h[k].data(), bytes, cudaMemcpyHostToDevice);
+            cudaMemcpy(ds, H->host.s[k].data(), bytes, cudaMemcpyHostToDevice);
+        }
+        st = build_plan(H);
+        if (st != LSH_OK) return fail(st);
+    }
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail(cuda_fail(e, "create sync"));
+    *out = H;
+    return LSH_OK;
+}
+
+extern "C" void lsh_destroy(lsh_handle* h) { free_handle(h); }
+
+extern "C" lsh_status lsh_check(const lsh_handle* h) {
+    if (!h) return LSH_ESTATE;
+    CK(cudaSetDevice(h->device));
+    CK(cudaDeviceSynchronize());
+    int flags = 0;
+    CK(cudaMemcpy(&flags, h->d_flags, sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemset(h->d_flags, 0, sizeof(int)));
+    if (flags & 3) return LSH_EOVERFLOW;
+    if (flags & 4) return LSH_EUNSUPPORTED;
+    return LSH_OK;
+}
+
+// ---------------------------------------------------------------------------
+// hashing
+// ---------------------------------------------------------------------------
+static lsh_status hash_impl(const lsh_handle* H, const float* X, int64_t n, int64_t ld, HashOut out, cudaStream_t s) {
+    const lsh_params& p = H->p;
+    if (out.bits && !is_e2lsh(p.scheme)) {
+        CK(cudaMemsetAsync(out.bits, 0, sizeof(uint32_t) * (size_t)n * ((p.m + 31) / 32), s));
+    }
+    if (out.codes && !is_e2lsh(p.scheme)) out.codes = nullptr;
+    if (out.bits && is_e2lsh(p.scheme)) out.bits = nullptr;
+    if (n == 0) return LSH_OK;
+    if (is_dense(p.scheme)) {
+        float* Y = out.proj;
+        if (!Y) CK(cudaMallocAsync((void**)&Y, sizeof(float) * (size_t)n * p.m, s));
+        timing_begin("dense_gemm", s);
+        cudaError_t e = launch_dense_gemm_f32(X, n, ld, H->d_R, p.m, (int)p.d, Y, s);
+        count_launch();
+        timing_end("dense_gemm", s);
+        if (e != cudaSuccess) return cuda_fail(e, "dense_gemm");
+        timing_begin("keys_from_proj", s);
+        e = launch_keys_from_proj(Y, n, p.m, p.L, p.K, H->disc, out, s);
+        count_launch();
+        timing_end("keys_from_proj", s);
+        if (e != cudaSuccess) return cuda_fail(e, "keys_from_proj");
+        if (!out.proj) CK(cudaFreeAsync(Y, s));
+        return LSH_OK;
+    }
+    if (!H->sketch_ok) return LSH_EUNSUPPORTED;
+    timing_begin("sketch", s);
+    cudaError_t e = launch_sketch(H->plan, H->disc, X, n, ld, out, H->num_sms, s);
+    count_launch();
+    timing_end("sketch", s);
+    if (e != cudaSuccess) return cuda_fail(e, "sketch");
+    return LSH_OK;
+}
+
+extern "C" lsh_status lsh_hash(const lsh_handle* h, const float* X, int64_t n, int64_t ld, uint64_t* keys,
+                               int32_t* codes, uint32_t* bits, float* proj, void* stream) {
+    if (!h) return LSH_ESTATE;
+    if (n < 0 || ld < h->p.d) return LSH_EDIM;
+    if (n > 0 && !X) return LSH_EDIM;
+    CK(cudaSetDevice(h->device));
+    return hash_impl(h, X, n, ld, HashOut{keys, codes, bits, proj}, (cudaStream_t)stream);
+}
+
+// ---------------------------------------------------------------------------
+// index
+// ---------------------------------------------------------------------------
+static lsh_status alloc_index(const lsh_handle* H, int64_t n, cudaStream_t s, lsh_index** out) {
+    lsh_index* I = new lsh_index();
+    I->h = H;
+    I->n = n;
+    I->stream = s;
+    I->L = H->p.L;
+    const int L = I->L;
+    const size_t b_ids = sizeof(uint32_t) * (size_t)L * n;
+    const size_t b_uk = sizeof(uint64_t) * (size_t)L * n;
+    const size_t b_off = sizeof(uint32_t) * (size_t)L * (n + 1);
+    const size_t b_nb = sizeof(uint32_t) * L;
+    const size_t total = b_uk + b_ids + b_off + b_nb + 64;
+    cudaError_t e = cudaMallocAsync(&I->mem, total, s);
+    if (e != cudaSuccess) {
+        delete I;
+        return cuda_fail(e, "index alloc");
+    }
+    char* base = (char*)I->mem;
+    I->dev.ukeys = (uint64_t*)base;
+    I->dev.ids = (uint32_t*)(base + b_uk);
+    I->dev.offs = (uint32_t*)(base + b_uk + b_ids);
+    I->dev.nb = (uint32_t*)(base + b_uk + b_ids + b_off);
+    cudaMallocHost(&I->nb_host, b_nb);
+    cudaEventCreateWithFlags(&I->done, cudaEventDisableTiming);
+    *out = I;
+    return LSH_OK;
+}
+
+static lsh_status group_impl(const lsh_handle* H, const uint64_t* keys, uint64_t* keys_scratch_b, int64_t n,
+                             int64_t id_base, lsh_index* I, cudaStream_t s) {
+    const int L = H->p.L;
+    GroupScratch sc{};
+    const size_t T = group_tiles(n);
+    const size_t b_keys = sizeof(uint64_t) * (size_t)L * n;
+    sc.overflow_cap = 1 << 16;
+    const size_t b_hist = sizeof(uint32_t) * (size_t)L * 256 * std::max<size_t>(T, 1);
+    const size_t b_aux = sizeof(uint32_t) * (size_t)L * (T + 1);
+    const size_t b_ovf = sizeof(uint32_t) * (1 + 3 * (size_t)sc.overflow_cap);
+    const size_t b_ids = sizeof(uint32_t) * (size_t)L * n;
+    const bool own_b = (keys_scratch_b == nullptr);
+    const size_t total = b_keys * (own_b ? 2 : 1) + b_ids + b_hist + b_aux + b_ovf + 256;
+    void* mem = nullptr;
+    if (n > 0) CK(cudaMallocAsync(&mem, total, s));
+    char* p = (char*)mem;
+    auto take = [&](size_t b) {
+        char* r = p;
+        p += (b + 127) / 128 * 128;
+        return r;
+    };
+    if (n > 0) {
+        sc.keys_a = (uint64_t*)take(b_keys);
+        sc.keys_b = own_b ? (uint64_t*)take(b_keys) : keys_scratch_b;
+        sc.ids_a = (uint32_t*)take(b_ids);
+        sc.hist = (uint32_t*)take(b_hist);
+        sc.tile_aux = (uint32_t*)take(b_aux);
+        sc.overflow = (uint32_t*)take(b_ovf);
+    }
+    cudaError_t e = launch_group(keys, n, L, (uint32_t)id_base, H->key_width, sc, I->dev, H->d_flags, s);
+    if (e != cudaSuccess) return cuda_fail(e, "group");
+    if (mem) CK(cudaFreeAsync(mem, s));
+    CK(cudaMemcpyAsync(I->nb_host, I->dev.nb, sizeof(uint32_t) * L, cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(I->done, s));
+    return LSH_OK;
+}
+
+extern "C" lsh_status lsh_group_keys(const lsh_handle* h, const uint64_t* keys, int64_t n, int64_t id_base,
+                                     lsh_index** out, void* stream) {
+    if (!h || !out) return LSH_ESTATE;
+    if (n < 0 || id_base < 0 || id_base + n > (1ll << 32)) return LSH_EDIM;
+    CK(cudaSetDevice(h->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    lsh_index* I = nullptr;
+    lsh_status st = alloc_index(h, n, s, &I);
+    if (st != LSH_OK) return st;
+    st = group_impl(h, keys, nullptr, n, id_base, I, s);
+    if (st != LSH_OK) {
+        lsh_index_destroy(I);
+        return st;
+    }
+    *out = I;
+    return LSH_OK;
+}
+
+extern "C" lsh_status lsh_build_index(const lsh_handle* h, const float* X, int64_t n, int64_t ld, int64_t id_base,
+                                      lsh_index** out, void* stream) {
+    if (!h || !out) return LSH_ESTATE;
+    if (n < 0 || ld < h->p.d || id_base < 0 || id_base + n > (1ll << 32)) return LSH_EDIM;
+    if (n > 0 && !X) return LSH_EDIM;
+    CK(cudaSetDevice(h->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    lsh_index* I = nullptr;
+    lsh_status st = alloc_index(h, n, s, &I);
+    if (st != LSH_OK) return st;
+    uint64_t* keys = nullptr;
+    if (n > 0) {
+        cudaError_t e = cudaMallocAsync((void**)&keys, sizeof(uint64_t) * (size_t)h->p.L * n, s);
+        if (e != cudaSuccess) {
+            lsh_index_destroy(I);
+            return cuda_fail(e, "keys alloc");
+        }
+    }
+    st = hash_impl(h, X, n, ld, HashOut{keys, nullptr, nullptr, nullptr}, s);
+    if (st == LSH_OK) st = group_impl(h, keys, keys, n, id_base, I, s);
+    if (keys) cudaFreeAsync(keys, s);
+    if (st != LSH_OK) {
+        lsh_index_destroy(I);
+        return st;
+    }
+    *out = I;
+    return LSH_OK;
+}
+
+extern "C" lsh_status lsh_index_view(const lsh_index* idx, int32_t t, const uint32_t** ids, const uint64_t** ukeys,
+                                     const uint32_t** offs, int64_t* nb) {
+    if (!idx) return LSH_ESTATE;
+    if (t < 0 || t >= idx->L) return LSH_EDIM;
+    CK(cudaEventSynchronize(idx->done));
+    const int64_t n = idx->n;
+    if (ids) *ids = idx->dev.ids + (int64_t)t * n;
+    if (ukeys) *ukeys = idx->dev.ukeys + (int64_t)t * n;
+    if (offs) *offs = idx->dev.offs + (int64_t)t * (n + 1);
+    if (nb) *nb = idx->nb_host[t];
+    return LSH_OK;
+}
+
+extern "C" int64_t lsh_index_size(const lsh_index* idx) { return idx ? idx->n : -1; }
+
+extern "C" void lsh_index_destroy(lsh_index* idx) {
+    if (!idx) return;
+    if (idx->done) cudaEventSynchronize(idx->done);
+    if (idx->mem) cudaFreeAsync(idx->mem, idx->stream);
+    if (idx->nb_host) cudaFreeHost(idx->nb_host);
+    if (idx->done) cudaEventDestroy(idx->done);
+    delete idx;
+}
+
+extern "C" lsh_status lsh_query_buckets(const lsh_handle* h, const lsh_index* idx, const float* Q, int64_t nq,
+                                        int64_t ld, int64_t* begin, int64_t* end, void* stream) {
+    if (!h || !idx || idx->h->p.L != h->p.L) return LSH_ESTATE;
+    if (nq < 0 || ld < h->p.d) return LSH_EDIM;
+    if (nq == 0) return LSH_OK;
+    if (!Q || !begin || !end) return LSH_EDIM;
+    CK(cudaSetDevice(h->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    uint64_t* qk = nullptr;
+    CK(cudaMallocAsync((void**)&qk, sizeof(uint64_t) * (size_t)h->p.L * nq, s));
+    lsh_status st = hash_impl(h, Q, nq, ld, HashOut{qk, nullptr, nullptr, nullptr}, s);
+    if (st == LSH_OK) {
+        timing_begin("lookup", s);
+        cudaError_t e = launch_lookup(qk, nq, h->p.L, idx->n, idx->dev, begin, end, s);
+        count_launch();
+        timing_end("lookup", s);
+        if (e != cudaSuccess) st = cuda_fail(e, "lookup");
+    }
+    cudaFreeAsync(qk, s);
+    return st;
+}
+
+extern "C" lsh_status lsh_index_counts(const lsh_index* idx, int32_t B, uint32_t* counts, void* stream) {
+    if (!idx) return LSH_ESTATE;
+    if (B < 1 || B > 20 || !counts) return LSH_EDIM;
+    CK(cudaSetDevice(idx->h->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    timing_begin("counts", s);
+    cudaError_t e = launch_counts(idx->dev, idx->n, idx->L, idx->h->key_width, B, counts, s);
+    count_launch();
+    timing_end("counts", s);
+    if (e != cudaSuccess) return cuda_fail(e, "counts");
+    return LSH_OK;
+}
+
+// ---------------------------------------------------------------------------
+// parameter export
+// ---------------------------------------------------------------------------
+static lsh_status export_from(const lsh_params* p, const HostTables& t, int32_t what, int32_t mode, void* buf,
+                              size_t* bytes) {
+    if (!bytes) return LSH_EDIM;
+    std::vector<unsigned char> out;
+    auto put = [&](const void* src, size_t nb) {
+        out.resize(nb);
+        if (nb) std::memcpy(out.data(), src, nb);
+    };
+    switch (what) {
+        case LSH_EXPORT_BUCKET:
+        case LSH_EXPORT_SIGN:
+        case LSH_EXPORT_COEFFS: {
+            if (is_dense(p->scheme) || mode < 0 || mode >= t.N) return LSH_EINVAL;
+            if (what == LSH_EXPORT_BUCKET) put(t.h[mode].data(), t.h[mode].size() * 4);
+            else if (what == LSH_EXPORT_SIGN) put(t.s[mode].data(), t.s[mode].size() * 4);
+            else {
+                uint64_t c[4] = {t.fb[mode].a, t.fb[mode].b, t.fs[mode].a, t.fs[mode].b};
+                put(c, sizeof(c));
+            }
+            break;
+        }
+        case LSH_EXPORT_OFFSETS: put(t.b.data(), t.b.size() * 4); break;
+        case LSH_EXPORT_GAUSSIAN:
+            if (!is_dense(p->scheme)) return LSH_EINVAL;
+            put(t.R.data(), t.R.size() * 2);
+            break;
+        case LSH_EXPORT_COORD: {
+            if (is_dense(p->scheme)) return LSH_EINVAL;
+            std::vector<int32_t> bin;
+            std::vector<int8_t> sg;
+            coordinate_map(p, t, bin, sg);
+            std::vector<int32_t> v(2 * p->d);
+            for (int64_t j = 0; j < p->d; ++j) {
+                v[j] = bin[j];
+                v[p->d + j] = sg[j];
+            }
+            put(v.data(), v.size() * 4);
+            break;
+        }
+        default: return LSH_EINVAL;
+    }
+    if (!buf || *bytes < out.size()) {
+        *bytes = out.size();
+        return LSH_EDIM;
+    }
+    *bytes = out.size();
+    if (!out.empty()) std::memcpy(buf, out.data(), out.size());
+    return LSH_OK;
+}
+
+extern "C" lsh_status lsh_export_host(const lsh_params* p, int32_t what, int32_t mode, void* host_buf,
+                                      size_t* bytes) {
+    lsh_status st = validate(p);
+    if (st != LSH_OK) return st;
+    HostTables t;
+    draw(p, t, what == LSH_EXPORT_GAUSSIAN);
+    return export_from(p, t, what, mode, host_buf, bytes);
+}
+
+extern "C" lsh_status lsh_get_params(const lsh_handle* h, int32_t what, int32_t mode, void* host_buf,
+                                     size_t* bytes) {
+    if (!h) return LSH_ESTATE;
+    CK(cudaSetDevice(h->device));
+    // Read back the DEVICE copies so the check covers what the kernels use.
+    HostTables t = h->host;
+    if (what == LSH_EXPORT_OFFSETS) CK(cudaMemcpy(t.b.data(), h->d_b, 4 * t.b.size(), cudaMemcpyDeviceToHost));
+    if (what == LSH_EXPORT_GAUSSIAN && h->d_R)
+        CK(cudaMemcpy(t.R.data(), h->d_R, 2 * t.R.size(), cudaMemcpyDeviceToHost));
+    if ((what == LSH_EXPORT_BUCKET || what == LSH_EXPORT_SIGN) && mode >= 0 && mode < (int)h->d_h.size()) {
+        CK(cudaMemcpy(t.h[mode].data(), h->d_h[mode], 4 * t.h[mode].size(), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(t.s[mode].data(), h->d_s[mode], 4 * t.s[mode].size(), cudaMemcpyDeviceToHost));
+    }
+    return export_from(&h->p, t, what, mode, host_buf, bytes);
+}

@@ -1,0 +1,452 @@
+// group.cu — K3/K5: grouping points into the buckets of each of the L tables
+// ("store every point p in bucket hbar_t(p)"; "arranging data
+// points into several bins of hash tables based on their hashcode")
+// and the bucket lookup of queries.  DESIGN.md §K3.
+//
+// Output order is canonical (reading B11): per table, ids sorted by (key, id),
+// i.e. buckets by ascending unsigned key, ids ascending inside a bucket.
+//
+//   1. stable LSD counting-sort passes on the top 16 significant key bits
+//      (8-bit digits; warp-level match_any ranking keeps each pass stable, so
+//      ids stay ascending inside equal digits),
+//   2. if keys are wider than 16 bits (E2LSH fingerprints, SRP with K > 16):
+//      stable sort of each equal-top-16 segment by the full key (segments are
+//      ~n/65536 long for fingerprints; long ones go to a CTA-level bitonic sort),
+//   3. run-length encoding -> ukeys / offs / nb.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.hpp"
+
+namespace lshb {
+
+constexpr int kTile = 2048;        // items per radix tile
+constexpr int kRT = 256;           // threads per radix block
+constexpr int kRounds = kTile / kRT;
+constexpr int kSegSmall = 64;      // segments up to this size: in-place insertion sort
+constexpr int kSegBig = 8192;      // CTA bitonic capacity
+
+size_t group_tiles(int64_t n) { return (size_t)((n + kTile - 1) / kTile); }
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t r;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+
+template <bool IMPLICIT_IDS>
+__global__ void __launch_bounds__(kRT) radix_upsweep(const uint64_t* __restrict__ keys, int64_t n, int sh,
+                                                     uint32_t* __restrict__ hist, int T) {
+    __shared__ uint32_t cnt[256];
+    const int t = blockIdx.y, tile = blockIdx.x;
+    cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const uint64_t* kt = keys + (int64_t)t * n;
+    for (int r = 0; r < kRounds; ++r) {
+        const int64_t i = (int64_t)tile * kTile + r * kRT + threadIdx.x;
+        if (i < n) atomicAdd(&cnt[(kt[i] >> sh) & 255], 1u);
+    }
+    __syncthreads();
+    hist[((int64_t)t * 256 + threadIdx.x) * T + tile] = cnt[threadIdx.x];
+}
+
+// Exclusive scan of `len` uint32 values per table (row stride `stride`) in place;
+// writes the total to total_out[t] if non-null and also at a[len] if write_end.
+__global__ void __launch_bounds__(1024) scan_rows(uint32_t* a, int64_t len, int64_t stride, uint32_t* total_out,
+                                                  int write_end) {
+    __shared__ uint32_t wsum[32];
+    __shared__ uint32_t carry_s;
+    uint32_t* row = a + (int64_t)blockIdx.x * stride;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) carry_s = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < len; base += 1024) {
+        const int64_t i = base + threadIdx.x;
+        const uint32_t v = i < len ? row[i] : 0u;
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t w = wsum[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += y;
+            }
+            wsum[lane] = w;
+        }
+        __syncthreads();
+        const uint32_t carry = carry_s;
+        const uint32_t excl = carry + (warp ? wsum[warp - 1] : 0u) + x - v;
+        if (i < len) row[i] = excl;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry_s = excl + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        if (total_out) total_out[blockIdx.x] = carry_s;
+        if (write_end) row[len] = carry_s;
+    }
+}
+
+template <bool IMPLICIT_IDS>
+__global__ void __launch_bounds__(kRT) radix_downsweep(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ iin,
+                                                       uint64_t* __restrict__ kout, uint32_t* __restrict__ iout,
+                                                       int64_t n, int sh, const uint32_t* __restrict__ hist, int T,
+                                                       uint32_t id_base) {
+    __shared__ uint32_t wcount[kRT / 32][256];
+    __shared__ uint32_t woff[kRT / 32][256];
+    __shared__ uint32_t run_base[256];
+    __shared__ uint32_t tile_off[256];
+    const int t = blockIdx.y, tile = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int w = 0; w < kRT / 32; ++w) wcount[w][threadIdx.x] = 0;
+    run_base[threadIdx.x] = 0;
+    tile_off[threadIdx.x] = hist[((int64_t)t * 256 + threadIdx.x) * T + tile];
+    __syncthreads();
+    const int64_t tb = (int64_t)t * n;
+    for (int r = 0; r < kRounds; ++r) {
+        const int64_t i = (int64_t)tile * kTile + r * kRT + threadIdx.x;
+        const bool valid = i < n;
+        uint64_t key = 0;
+        uint32_t id = 0;
+        uint32_t dg = 256;
+        if (valid) {
+            key = kin[tb + i];
+            id = IMPLICIT_IDS ? id_base + (uint32_t)i : iin[tb + i];
+            dg = (uint32_t)(key >> sh) & 255u;
+        }
+        const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+        const uint32_t rank = __popc(peers & lanemask_lt());
+        if (valid && rank == 0) wcount[warp][dg] = __popc(peers);
+        __syncthreads();
+        {
+            const int dd = threadIdx.x;
+            uint32_t acc = run_base[dd];
+#pragma unroll
+            for (int w = 0; w < kRT / 32; ++w) {
+                woff[w][dd] = acc;
+                acc += wcount[w][dd];
+                wcount[w][dd] = 0;
+            }
+            run_base[dd] = acc;
+        }
+        __syncthreads();
+        if (valid) {
+            const uint32_t pos = tile_off[dg] + woff[warp][dg] + rank;
+            kout[tb + pos] = key;
+            iout[tb + pos] = id;
+        }
+    }
+}
+
+__device__ __forceinline__ bool kless(uint64_t ka, uint32_t ia, uint64_t kb, uint32_t ib) {
+    return ka < kb || (ka == kb && ia < ib);
+}
+
+// Segments of equal top-16 significant bits: stable sort by the full key.
+__global__ void segsort_small(uint64_t* __restrict__ keys, uint32_t* __restrict__ ids, int64_t n, int L, int pre_sh,
+                              uint32_t* overflow, int cap) {
+    const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gi >= (int64_t)L * n) return;
+    const int t = (int)(gi / n);
+    const int64_t i = gi % n;
+    uint64_t* k = keys + (int64_t)t * n;
+    uint32_t* d = ids + (int64_t)t * n;
+    const uint64_t pre = k[i] >> pre_sh;
+    if (i > 0 && (k[i - 1] >> pre_sh) == pre) return;  // not a segment head
+    int64_t j = i + 1;
+    while (j < n && (k[j] >> pre_sh) == pre && j - i <= kSegSmall) ++j;
+    if (j - i > kSegSmall) {
+        while (j < n && (k[j] >> pre_sh) == pre) ++j;
+        const uint32_t slot = atomicAdd(overflow, 1u);
+        if ((int)slot < cap) {
+            overflow[1 + 3 * slot] = (uint32_t)t;
+            overflow[2 + 3 * slot] = (uint32_t)i;
+            overflow[3 + 3 * slot] = (uint32_t)j;
+        }
+        return;
+    }
+    // insertion sort (stable: only strictly larger keys move right)
+    for (int64_t a = i + 1; a < j; ++a) {
+        const uint64_t kv = k[a];
+        const uint32_t iv = d[a];
+        int64_t b = a - 1;
+        while (b >= i && k[b] > kv) {
+            k[b + 1] = k[b];
+            d[b + 1] = d[b];
+            --b;
+        }
+        k[b + 1] = kv;
+        d[b + 1] = iv;
+    }
+}
+
+__global__ void __launch_bounds__(1024) segsort_big(uint64_t* __restrict__ keys, uint32_t* __restrict__ ids, int64_t n,
+                                                    const uint32_t* overflow, int cap, int* flags) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    uint64_t* sk = reinterpret_cast<uint64_t*>(sm);
+    uint32_t* si = reinterpret_cast<uint32_t*>(sm + kSegBig * sizeof(uint64_t));
+    const uint32_t count = min(overflow[0], (uint32_t)cap);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && overflow[0] > (uint32_t)cap) atomicOr(flags, 4);
+    for (uint32_t e = blockIdx.x; e < count; e += gridDim.x) {
+        const int t = overflow[1 + 3 * e];
+        const int64_t lo = overflow[2 + 3 * e], hi = overflow[3 + 3 * e];
+        uint64_t* k = keys + (int64_t)t * n;
+        uint32_t* d = ids + (int64_t)t * n;
+        const int64_t len = hi - lo;
+        if (len > kSegBig) {
+            // Only supported when every key is equal (then already id-ascending).
+            __shared__ int neq;
+            if (threadIdx.x == 0) neq = 0;
+            __syncthreads();
+            for (int64_t a = lo + 1 + threadIdx.x; a < hi; a += blockDim.x)
+                if (k[a] != k[lo]) neq = 1;
+            __syncthreads();
+            if (neq && threadIdx.x == 0) atomicOr(flags, 4);
+            __syncthreads();
+            continue;
+        }
+        int P = 1;
+        while (P < len) P <<= 1;
+        for (int a = threadIdx.x; a < P; a += blockDim.x) {
+            if (a < len) {
+                sk[a] = k[lo + a];
+                si[a] = d[lo + a];
+            } else {
+                sk[a] = ~0ull;
+                si[a] = 0xffffffffu;
+            }
+        }
+        __syncthreads();
+        for (int size = 2; size <= P; size <<= 1) {
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int a = threadIdx.x; a < P; a += blockDim.x) {
+                    const int b = a ^ stride;
+                    if (b > a) {
+                        const bool up = (a & size) == 0;
+                        const bool sw = up ? kless(sk[b], si[b], sk[a], si[a]) : kless(sk[a], si[a], sk[b], si[b]);
+                        if (sw) {
+                            const uint64_t tk = sk[a];
+                            sk[a] = sk[b];
+                            sk[b] = tk;
+                            const uint32_t ti = si[a];
+                            si[a] = si[b];
+                            si[b] = ti;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (int a = threadIdx.x; a < len; a += blockDim.x) {
+            k[lo + a] = sk[a];
+            d[lo + a] = si[a];
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kRT) rle_count(const uint64_t* __restrict__ keys, int64_t n, uint32_t* tile_aux,
+                                                 int T) {
+    __shared__ uint32_t c;
+    const int t = blockIdx.y, tile = blockIdx.x;
+    if (threadIdx.x == 0) c = 0;
+    __syncthreads();
+    const uint64_t* k = keys + (int64_t)t * n;
+    uint32_t local = 0;
+    for (int r = 0; r < kRounds; ++r) {
+        const int64_t i = (int64_t)tile * kTile + r * kRT + threadIdx.x;
+        if (i < n && (i == 0 || k[i] != k[i - 1])) ++local;
+    }
+    atomicAdd(&c, local);
+    __syncthreads();
+    if (threadIdx.x == 0) tile_aux[(int64_t)t * (T + 1) + tile] = c;
+}
+
+__global__ void __launch_bounds__(kRT) rle_write(const uint64_t* __restrict__ keys, int64_t n,
+                                                 const uint32_t* tile_aux, int T, IndexDev out) {
+    __shared__ uint32_t wsum[kRT / 32];
+    __shared__ uint32_t base_s;
+    const int t = blockIdx.y, tile = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t* k = keys + (int64_t)t * n;
+    if (threadIdx.x == 0) base_s = tile_aux[(int64_t)t * (T + 1) + tile];
+    __syncthreads();
+    for (int r = 0; r < kRounds; ++r) {
+        const int64_t i = (int64_t)tile * kTile + r * kRT + threadIdx.x;
+        const bool head = i < n && (i == 0 || k[i] != k[i - 1]);
+        const uint32_t ball = __ballot_sync(0xffffffffu, head);
+        if (lane == 0) wsum[warp] = __popc(ball);
+        __syncthreads();
+        uint32_t before = base_s;
+        for (int w = 0; w < warp; ++w) before += wsum[w];
+        if (head) {
+            const uint32_t b = before + __popc(ball & lanemask_lt());
+            out.ukeys[(int64_t)t * n + b] = k[i];
+            out.offs[(int64_t)t * (n + 1) + b] = (uint32_t)i;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t s = 0;
+            for (int w = 0; w < kRT / 32; ++w) s += wsum[w];
+            base_s += s;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void rle_finish(IndexDev out, const uint32_t* tile_aux, int T, int64_t n, int L) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= L) return;
+    const uint32_t nb = tile_aux[(int64_t)t * (T + 1) + T];
+    out.nb[t] = nb;
+    out.offs[(int64_t)t * (n + 1) + nb] = (uint32_t)n;
+}
+
+cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_base, int W, GroupScratch& sc,
+                         IndexDev& out, int* flags, cudaStream_t s) {
+    cudaError_t e;
+    if (n == 0) {
+        e = cudaMemsetAsync(out.nb, 0, sizeof(uint32_t) * L, s);
+        if (e != cudaSuccess) return e;
+        return cudaMemsetAsync(out.offs, 0, sizeof(uint32_t) * L * (n + 1), s);
+    }
+    const int T = (int)group_tiles(n);
+    const dim3 g2(T, L);
+    // digit shifts covering the top 16 significant bits, low digit first
+    int shifts[2];
+    int npass;
+    if (W <= 8) {
+        shifts[0] = 0;
+        npass = 1;
+    } else if (W <= 16) {
+        shifts[0] = 0;
+        shifts[1] = 8;
+        npass = 2;
+    } else {
+        shifts[0] = W - 16;
+        shifts[1] = W - 8;
+        npass = 2;
+    }
+    // pass outputs alternate keys_a, keys_b (keys_b may alias the input keys:
+    // the input is fully consumed by pass 0, which writes keys_a)
+    const uint64_t* kin = keys;
+    const uint32_t* iin = nullptr;
+    for (int p = 0; p < npass; ++p) {
+        const bool lastp = (p == npass - 1);
+        uint64_t* kout = (p == 0) ? sc.keys_a : sc.keys_b;
+        uint32_t* iout = lastp ? out.ids : sc.ids_a;
+        timing_begin("radix_upsweep", s);
+        if (p == 0) radix_upsweep<true><<<g2, kRT, 0, s>>>(kin, n, shifts[p], sc.hist, T);
+        else radix_upsweep<false><<<g2, kRT, 0, s>>>(kin, n, shifts[p], sc.hist, T);
+        count_launch();
+        timing_end("radix_upsweep", s);
+        timing_begin("radix_scan", s);
+        scan_rows<<<L, 1024, 0, s>>>(sc.hist, (int64_t)256 * T, (int64_t)256 * T, nullptr, 0);
+        count_launch();
+        timing_end("radix_scan", s);
+        timing_begin("radix_downsweep", s);
+        if (p == 0)
+            radix_downsweep<true><<<g2, kRT, 0, s>>>(kin, iin, kout, iout, n, shifts[p], sc.hist, T, id_base);
+        else
+            radix_downsweep<false><<<g2, kRT, 0, s>>>(kin, iin, kout, iout, n, shifts[p], sc.hist, T, id_base);
+        count_launch();
+        timing_end("radix_downsweep", s);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        kin = kout;
+        iin = iout;
+    }
+    uint64_t* sorted = (npass == 1) ? sc.keys_a : sc.keys_b;
+    if (W > 16) {
+        timing_begin("segsort", s);
+        e = cudaMemsetAsync(sc.overflow, 0, sizeof(uint32_t), s);
+        if (e != cudaSuccess) return e;
+        const int64_t tot = (int64_t)L * n;
+        segsort_small<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(sorted, out.ids, n, L, W - 16, sc.overflow,
+                                                                   sc.overflow_cap);
+        count_launch();
+        const size_t smem = kSegBig * (sizeof(uint64_t) + sizeof(uint32_t));
+        cudaFuncSetAttribute(segsort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        segsort_big<<<148, 1024, smem, s>>>(sorted, out.ids, n, sc.overflow, sc.overflow_cap, flags);
+        count_launch();
+        timing_end("segsort", s);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    timing_begin("rle", s);
+    rle_count<<<g2, kRT, 0, s>>>(sorted, n, sc.tile_aux, T);
+    count_launch();
+    scan_rows<<<L, 1024, 0, s>>>(sc.tile_aux, T, T + 1, nullptr, 1);
+    count_launch();
+    rle_write<<<g2, kRT, 0, s>>>(sorted, n, sc.tile_aux, T, out);
+    count_launch();
+    rle_finish<<<(L + 127) / 128, 128, 0, s>>>(out, sc.tile_aux, T, n, L);
+    count_launch();
+    timing_end("rle", s);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// K5: bucket lookup of query keys ("collect the index of all the
+// elements ... hashed in hbar_t(q)").
+// ---------------------------------------------------------------------------
+__global__ void lookup_kernel(const uint64_t* __restrict__ qkeys, int64_t nq, int L, int64_t n, IndexDev idx,
+                              int64_t* __restrict__ begin, int64_t* __restrict__ end) {
+    const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gi >= nq * L) return;
+    const int64_t q = gi / L;
+    const int t = (int)(gi % L);
+    const uint64_t key = qkeys[(int64_t)t * nq + q];
+    const uint64_t* uk = idx.ukeys + (int64_t)t * n;
+    const uint32_t* of = idx.offs + (int64_t)t * (n + 1);
+    int64_t lo = 0, hi = idx.nb[t];
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (uk[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    int64_t b, e;
+    if (lo < idx.nb[t] && uk[lo] == key) {
+        b = of[lo];
+        e = of[lo + 1];
+    } else {
+        b = e = of[lo];
+    }
+    begin[q * L + t] = b;
+    end[q * L + t] = e;
+}
+
+cudaError_t launch_lookup(const uint64_t* qkeys, int64_t nq, int L, int64_t n, const IndexDev& idx, int64_t* begin,
+                          int64_t* end, cudaStream_t s) {
+    if (nq == 0) return cudaSuccess;
+    const int64_t tot = nq * L;
+    lookup_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(qkeys, nq, L, n, idx, begin, end);
+    return cudaGetLastError();
+}
+
+__global__ void counts_kernel(IndexDev idx, int64_t n, int L, int W, int B, uint32_t* counts) {
+    const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gi >= (int64_t)L * n) return;
+    const int t = (int)(gi / n);
+    const int64_t b = gi % n;
+    if (b >= idx.nb[t]) return;
+    const uint64_t key = idx.ukeys[(int64_t)t * n + b];
+    const uint64_t bin = W > B ? (key >> (W - B)) : key;
+    const uint32_t sz = idx.offs[(int64_t)t * (n + 1) + b + 1] - idx.offs[(int64_t)t * (n + 1) + b];
+    atomicAdd(&counts[((int64_t)t << B) + bin], sz);
+}
+
+cudaError_t launch_counts(const IndexDev& idx, int64_t n, int L, int W, int B, uint32_t* counts, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(uint32_t) * ((size_t)L << B), s);
+    if (e != cudaSuccess || n == 0) return e;
+    const int64_t tot = (int64_t)L * n;
+    counts_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(idx, n, L, W, B, counts);
+    return cudaGetLastError();
+}
+
+}  // namespace lshb

@@ -1,0 +1,85 @@
+// internal.hpp — structures shared by the host core (api.cu) and the kernel
+// launchers (sketch.cu, group.cu, dense.cu).  Not part of the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lshb {
+
+// Fingerprint constants of reading B10 (FNV-1a-64 + SplitMix64 finaliser).
+#define LSHB_FNV_OFFSET 0xcbf29ce484222325ull
+#define LSHB_FNV_PRIME 0x100000001b3ull
+
+// ---------------------------------------------------------------------------
+// Sparse one-nonzero-per-column projection (CS and HCS), DESIGN.md §K1.
+// The host planner turns the per-coordinate (bin, sign) map of Def. CS
+// / Def. HCS into, per coordinate chunk and per
+// bin, the list of contributing coordinates ("entries"), sorted ascending.
+// Entry encoding: bits 0..30 = word offset of the coordinate inside the staged
+// transposed tile (k>>2)*129 + (k&3)*32, bit 31 = sign (1 = negative).
+// ---------------------------------------------------------------------------
+struct SketchPlanDev {
+    int d, m, L, K;
+    int Q;            // coordinates per chunk (64 * VPT)
+    int vpt;          // float4 registers per thread (template selector)
+    int nchunks;
+    const uint32_t* entries;  // d entries
+    const int32_t* bin_ptr;   // [nchunks][m+1]
+};
+
+struct DiscretizeDev {
+    int e2lsh;                // 1: E2LSH floor codes + fingerprint keys; 0: SRP bits
+    float c_scale;            // sqrt(m)/w (CS/HCS), 1/w (dense)
+    const float* c_off;       // [m] b_l / w  (E2LSH)
+    int* flags;               // sticky device status (bit 0: int32 overflow, bit 1: NaN)
+};
+
+struct HashOut {
+    uint64_t* keys;   // [L][n]
+    int32_t* codes;   // [n][m]
+    uint32_t* bits;   // [n][ceil(m/32)]
+    float* proj;      // [n][m]
+};
+
+// Launchers (return cudaError_t of the launch).
+cudaError_t launch_sketch(const SketchPlanDev& plan, const DiscretizeDev& disc, const float* X, int64_t n,
+                          int64_t ld, HashOut out, int num_sms, cudaStream_t s);
+size_t sketch_smem_bytes(int Q, int m, int nchunks);
+
+cudaError_t launch_dense_gemm_f32(const float* X, int64_t n, int64_t ld, const uint16_t* Rbf16, int m, int d,
+                                  float* Y, cudaStream_t s);
+cudaError_t launch_keys_from_proj(const float* Y, int64_t n, int m, int L, int K, const DiscretizeDev& disc,
+                                  HashOut out, cudaStream_t s);
+
+// Grouping.
+struct GroupScratch {
+    uint64_t* keys_a;
+    uint64_t* keys_b;
+    uint32_t* ids_a;
+    uint32_t* ids_b;
+    uint32_t* hist;       // [L][256][tiles] (reused per pass)
+    uint32_t* tile_aux;   // [L][tiles+1]
+    uint32_t* overflow;   // [1 + 3 * cap] (count, then (t, lo, hi) triples)
+    int overflow_cap;
+};
+struct IndexDev {
+    uint32_t* ids;    // [L][n]
+    uint64_t* ukeys;  // [L][n]  (capacity n per table)
+    uint32_t* offs;   // [L][n+1]
+    uint32_t* nb;     // [L]
+};
+size_t group_tiles(int64_t n);
+cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_base, int key_width,
+                         GroupScratch& sc, IndexDev& out, int* flags, cudaStream_t s);
+cudaError_t launch_lookup(const uint64_t* qkeys, int64_t nq, int L, int64_t n, const IndexDev& idx,
+                          int64_t* begin, int64_t* end, cudaStream_t s);
+cudaError_t launch_counts(const IndexDev& idx, int64_t n, int L, int width, int B, uint32_t* counts,
+                          cudaStream_t s);
+
+// Instrumentation (api.cu): every launch goes through these.
+void timing_begin(const char* name, cudaStream_t s);
+void timing_end(const char* name, cudaStream_t s);
+void count_launch();
+
+}  // namespace lshb

@@ -1,0 +1,233 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by
+element on the same seeded inputs.  Marked `gpu`: runs on a B200 only."""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import lsh  # noqa: E402
+import synth  # noqa: E402
+
+from . import parity  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2503_06737_b200 as pk
+    pk.lib()
+    yield
+
+
+def _handle(p: lsh.Params):
+    import paper_2503_06737_b200 as pk
+    kw = dict(mode_d=p.mode_d, mode_m=p.mode_m) if lsh.is_hcs(p.scheme) else {}
+    return pk.LSH(p.scheme, p.d, p.m, p.L, p.K, p.w, p.seed, **kw)
+
+
+def _params(cfg: synth.Config, scheme: str) -> lsh.Params:
+    kw = dict(mode_d=cfg.mode_d, mode_m=cfg.mode_m) if scheme.startswith("HCS") else {}
+    return lsh.Params(scheme, d=cfg.d, m=cfg.m, L=cfg.L, K=cfg.K, w=cfg.w, seed=cfg.hash_seed, **kw)
+
+
+def _compare(p: lsh.Params, X_dev, X_np, h=None, rows=None, report=None):
+    """Hash X_dev on the GPU, compare proj / codes|bits / keys with the oracle on X_np."""
+    h = h or _handle(p)
+    out = h.hash(X_dev, keys=True, codes=True, bits=True, proj=True)
+    torch.cuda.synchronize()
+    h.check()
+    sel = slice(None) if rows is None else rows
+    gk = out["keys"].cpu().numpy()[:, sel]
+    gp = out["proj"].cpu().numpy()[sel]
+    t = lsh.make_tables(p)
+    ref = lsh.hash_points(p, t, X_np)
+    pr = parity.check_proj(gp, ref["proj"], parity.sigma(p, t, X_np))
+    assert pr["bad"] == 0 and pr["bad_empty"] == 0, pr
+    if lsh.is_e2lsh(p.scheme):
+        cr = parity.check_codes(p, ref, gpu_codes=out["codes"].cpu().numpy()[sel])
+    else:
+        cr = parity.check_codes(p, ref, gpu_bits=parity.unpack_bits(out["bits"].cpu().numpy()[sel], p.m))
+    assert cr["mismatch_outside_exempt"] == 0, cr
+    kr = parity.check_keys(p, ref, gk)
+    assert kr["mismatch_outside_exempt"] == 0, kr
+    if report is not None:
+        report.update(proj=pr, codes=cr, keys=kr)
+    return h, out, ref
+
+
+@pytest.mark.parametrize("cfg,scheme", [("C1", "CS_E2LSH"), ("C1", "CS_SRP"), ("C2", "CS_E2LSH"),
+                                        ("C2", "CS_SRP"), ("C2", "E2LSH"), ("C2", "SRP"),
+                                        ("C3", "HCS_E2LSH"), ("C3", "HCS_SRP"), ("C3", "CS_E2LSH"),
+                                        ("C3", "CS_SRP")])
+def test_config_full_n(cfg, scheme):
+    c = synth.CONFIGS[cfg]
+    p = _params(c, scheme)
+    X = synth.rows(c, 0, c.n, device="cuda")
+    _compare(p, X, X.cpu().numpy())
+
+
+@pytest.mark.parametrize("scheme", ["CS_E2LSH", "CS_SRP"])
+def test_c4_full_size_sampled(scheme):
+    """C4 at full n=1e6 in the bench's launch configuration; oracle on sampled rows."""
+    c = synth.CONFIGS["C4"]
+    p = _params(c, scheme)
+    X = synth.rows(c, 0, c.n, device="cuda")
+    h = _handle(p)
+    out = h.hash(X, keys=True, codes=True, bits=True, proj=True)
+    torch.cuda.synchronize()
+    g = np.random.default_rng(0)
+    rows = np.concatenate([np.arange(4096), np.sort(g.choice(np.arange(4096, c.n), 4096, replace=False))])
+    Xs = X[torch.from_numpy(rows).cuda()].cpu().numpy()
+    t = lsh.make_tables(p)
+    ref = lsh.hash_points(p, t, Xs)
+    pr = parity.check_proj(out["proj"][torch.from_numpy(rows).cuda()].cpu().numpy(), ref["proj"],
+                           parity.sigma(p, t, Xs))
+    assert pr["bad"] == 0 and pr["bad_empty"] == 0, pr
+    kr = parity.check_keys(p, ref, out["keys"][:, torch.from_numpy(rows).cuda()].cpu().numpy())
+    assert kr["mismatch_outside_exempt"] == 0, kr
+
+
+@pytest.mark.parametrize("n", [0, 1, 31, 33, 1000])
+@pytest.mark.parametrize("scheme,d,m,L,K,kw", [
+    ("CS_E2LSH", 64, 16, 2, 8, {}),
+    ("CS_SRP", 50, 24, 3, 8, {}),                                   # d % 4 != 0: scalar staging path
+    ("HCS_E2LSH", 60, 24, 3, 8, dict(mode_d=(4, 4, 4), mode_m=(2, 3, 4))),   # zero padding, unequal modes
+    ("CS_E2LSH", 1500, 64, 4, 16, {}),                              # multi-chunk, ragged last chunk
+    ("SRP", 37, 40, 5, 8, {}),
+])
+def test_edge_shapes(n, scheme, d, m, L, K, kw):
+    p = lsh.Params(scheme, d=d, m=m, L=L, K=K, w=2.5, seed=7, **kw)
+    X = synth.gaussian_rows_like(n, d, 3, device="cuda")
+    if n == 0:
+        h = _handle(p)
+        out = h.hash(X, keys=True)
+        assert out["keys"].shape == (L, 0)
+        return
+    _compare(p, X, X.cpu().numpy())
+
+
+def test_padded_rows_and_unaligned_pointer():
+    p = lsh.Params("CS_E2LSH", d=64, m=16, L=2, K=8, w=4.0, seed=1)
+    big = synth.gaussian_rows_like(300, 72, 5, device="cuda")
+    X = big[:, :64]                     # ld = 72 > d
+    _compare(p, X, X.cpu().numpy())
+    X2 = big.view(-1)[1:1 + 299 * 72].view(299, 72)[:, :64]  # misaligned base -> scalar path
+    _compare(p, X2, X2.cpu().numpy())
+
+
+def test_zero_and_duplicate_points():
+    for scheme in ("CS_E2LSH", "CS_SRP", "HCS_SRP"):
+        kw = dict(mode_d=(8, 8), mode_m=(4, 4)) if scheme.startswith("HCS") else {}
+        p = lsh.Params(scheme, d=64, m=16, L=1, K=16, w=4.0, seed=2, **kw)
+        X = synth.gaussian_rows_like(100, 64, 9, device="cuda")
+        X[0:10] = 0
+        X[20:40] = X[19]
+        _h, out, ref = _compare(p, X, X.cpu().numpy())
+        keys = out["keys"].cpu().numpy()
+        assert np.all(keys[:, 20:40] == keys[:, 19:20])
+
+
+def test_overflow_flag():
+    import paper_2503_06737_b200 as pk
+    p = lsh.Params("CS_E2LSH", d=64, m=16, L=2, K=8, w=1e-6, seed=1)
+    h = _handle(p)
+    X = torch.full((32, 64), 1e6, device="cuda")
+    h.hash(X, keys=True)
+    with pytest.raises(pk.LshError) as e:
+        h.check()
+    assert e.value.status == 5
+    h.check()  # sticky flag cleared
+
+
+def test_device_params_equal_oracle():
+    for scheme, kw in [("CS_E2LSH", {}), ("HCS_SRP", dict(mode_d=(16, 16, 16), mode_m=(8, 8, 8))),
+                       ("E2LSH", {})]:
+        d = 4096 if scheme.startswith("HCS") else 784
+        p = lsh.Params(scheme, d=d, m=512 if scheme.startswith("HCS") else 160,
+                       L=32 if scheme.startswith("HCS") else 10, K=16, w=4.0, seed=3, **kw)
+        h = _handle(p)
+        t = lsh.make_tables(p)
+        assert np.array_equal(h.get_params("offsets").view(np.uint32), t.b.view(np.uint32))
+        if lsh.is_dense(scheme):
+            got = (h.get_params("gaussian").astype(np.uint32) << 16).view(np.float32)
+            assert np.array_equal(got, t.R.astype(np.float32).ravel())
+        else:
+            for k in range(p.N):
+                assert np.array_equal(h.get_params("bucket", k), t.h[k])
+                assert np.array_equal(h.get_params("sign", k), t.s[k])
+
+
+# ---------------------------------------------------------------- grouping --
+
+def _check_index(idx, ref_tables, L):
+    for tt in range(L):
+        ids, uk, of = (x.cpu().numpy() for x in idx.view(tt))
+        r = ref_tables[tt]
+        assert np.array_equal(uk.astype(np.uint64), r.ukeys), tt
+        assert np.array_equal(of.astype(np.uint32), r.offs), tt
+        assert np.array_equal(ids.astype(np.uint32), r.ids), tt
+
+
+@pytest.mark.parametrize("scheme,K,n", [("CS_E2LSH", 16, 60000), ("CS_SRP", 16, 60000), ("CS_SRP", 8, 5000),
+                                        ("CS_SRP", 24, 20000), ("CS_E2LSH", 8, 1)])
+def test_group_keys_bit_exact_given_oracle_keys(scheme, K, n):
+    L = 4
+    p = lsh.Params(scheme, d=64, m=L * K, L=L, K=K, w=4.0, seed=0)
+    h = _handle(p)
+    g = np.random.default_rng(1)
+    if lsh.is_e2lsh(scheme):
+        keys = g.integers(0, 2 ** 63, (L, n), dtype=np.int64).astype(np.uint64) * np.uint64(2) + \
+            g.integers(0, 2, (L, n)).astype(np.uint64)
+        keys[:, : n // 3] = keys[:, :1]          # a large equal-key bucket
+        keys[:, n // 2: n // 2 + 100] = (keys[:, n // 2: n // 2 + 100] >> np.uint64(40)) << np.uint64(40)
+    else:
+        keys = g.integers(0, 1 << K, (L, n)).astype(np.uint64)
+        keys[:, ::7] = 5                          # skewed bucket
+    idx = h.group_keys(torch.from_numpy(keys.view(np.int64)).cuda().view(torch.uint64), id_base=17)
+    ref = lsh.group(keys, id_base=17)
+    _check_index(idx, ref, L)
+    h.check()
+
+
+@pytest.mark.parametrize("cfg,scheme", [("C2", "CS_E2LSH"), ("C2", "CS_SRP"), ("C3", "HCS_SRP"),
+                                        ("C1", "CS_E2LSH")])
+def test_build_index_and_query(cfg, scheme):
+    c = synth.CONFIGS[cfg]
+    p = _params(c, scheme)
+    h = _handle(p)
+    X = synth.rows(c, 0, c.n, device="cuda")
+    keys = h.hash(X, keys=True)["keys"].cpu().numpy()
+    idx = h.build_index(X, id_base=0)
+    _check_index(idx, lsh.group(keys), p.L)
+    # queries: a subset of the indexed points plus fresh points
+    Q = torch.cat([X[:500], synth.gaussian_rows_like(100, c.d, 77, device="cuda").abs()])
+    b, e = h.query_buckets(idx, Q)
+    qk = h.hash(Q, keys=True)["keys"].cpu().numpy()
+    ref = lsh.group(keys)
+    b, e = b.cpu().numpy(), e.cpu().numpy()
+    for q in range(Q.shape[0]):
+        for tt in range(p.L):
+            assert (b[q, tt], e[q, tt]) == lsh.lookup(ref[tt], int(qk[tt, q]))
+    for q in range(500):  # self-retrieval
+        for tt in range(p.L):
+            ids = idx.view(tt)[0].cpu().numpy()[b[q, tt]:e[q, tt]]
+            assert q in ids.tolist()
+    # coarse counts (multi-GPU exchange)
+    for B in (4, 12):
+        cnt = idx.counts(B).cpu().numpy().astype(np.uint32)
+        assert np.array_equal(cnt, lsh.coarse_counts(p, keys, B))
+
+
+def test_empty_index():
+    p = lsh.Params("CS_SRP", d=64, m=16, L=2, K=8, seed=0)
+    h = _handle(p)
+    idx = h.build_index(torch.zeros((0, 64), device="cuda"))
+    ids, uk, of = idx.view(0)
+    assert ids.numel() == 0 and uk.numel() == 0 and of.cpu().tolist() == [0]

@@ -237,3 +237,14 @@ def test_no_fingerprint_merges_on_sample():
     X = np.random.default_rng(10).random((1000, 64)).astype(np.float32)
     out = lsh.hash_points(p, t, X)
     assert lsh.fingerprint_merges(out["codes"], out["keys"], 2, 8) == 0
+
+
+def test_vectorised_keys_equal_scalar_fingerprint():
+    g = np.random.default_rng(11)
+    codes = g.integers(-300, 300, (50, 32))
+    codes[0] = 0
+    codes[1, :5] = [-(1 << 31), (1 << 31) - 1, -1, 1, 0]
+    keys = lsh.e2lsh_keys(codes, 2, 16)
+    for i in range(50):
+        for t in range(2):
+            assert int(keys[t, i]) == lsh.fingerprint(codes[i, t * 16:(t + 1) * 16].tolist())
