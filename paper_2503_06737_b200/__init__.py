@@ -165,7 +165,7 @@ class _DevArray:
     """__cuda_array_interface__ over library-owned device memory (zero-copy view)."""
 
     def __init__(self, ptr: int, shape, typestr: str, owner):
-        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), True),
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
                                          "version": 3, "strides": None}
         self._owner = owner
 

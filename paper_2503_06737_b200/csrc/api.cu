@@ -253,8 +253,9 @@ struct lsh_handle {
     int key_width = 64;
     SketchPlanDev plan{};
     DiscretizeDev disc{};
-    uint32_t* d_entries = nullptr;
-    int32_t* d_binptr = nullptr;
+    uint16_t* d_entries = nullptr;
+    uint32_t* d_binptr = nullptr;
+    uint32_t* d_signs = nullptr;
     float* d_coff = nullptr;
     uint16_t* d_R = nullptr;
     int* d_flags = nullptr;
@@ -280,45 +281,42 @@ static lsh_status build_plan(lsh_handle* H) {
     std::vector<int8_t> sgn;
     coordinate_map(p, H->host, bin, sgn);
     const int d = (int)p->d, m = p->m;
-    int vpt = 0;
-    for (int v : {1, 2, 4, 8, 16})
-        if (64 * v >= d) {
-            vpt = v;
-            break;
-        }
-    int nchunks = 1;
-    if (!vpt) {
-        // chunked: partial bins of the tile live in shared memory
-        vpt = 16;
-        if (sketch_smem_bytes(64 * vpt, m, 2) > 232448) vpt = 8;
-        nchunks = (d + 64 * vpt - 1) / (64 * vpt);
-        if (sketch_smem_bytes(64 * vpt, m, nchunks) > 232448) {
-            H->sketch_ok = false;
-            return LSH_OK;
-        }
-    }
+    const int vpt = d <= 64 ? 1 : (d <= 256 ? 4 : 16);
     const int Q = 64 * vpt;
-    std::vector<int32_t> bin_ptr((size_t)nchunks * (m + 1), 0);
-    std::vector<uint32_t> entries(d);
+    const int nchunks = (d + Q - 1) / Q;
+    if (sketch_smem_bytes(Q, m, d, nchunks) > 232448) {
+        H->sketch_ok = false;  // needs the structured HCS path (not in this build)
+        return LSH_OK;
+    }
+    std::vector<uint32_t> bin_ptr((size_t)nchunks * (m + 1), 0);
+    std::vector<uint16_t> entries(d);
+    std::vector<uint32_t> sign_bits((d + 31) / 32, 0);
+    for (int j = 0; j < d; ++j)
+        if (sgn[j] < 0) sign_bits[j >> 5] |= 1u << (j & 31);
     for (int c = 0; c < nchunks; ++c) {
         const int j0 = c * Q, j1 = std::min(d, (c + 1) * Q);
-        int32_t* bp = bin_ptr.data() + (size_t)c * (m + 1);
-        std::vector<int32_t> cnt(m + 1, 0);
+        uint32_t* bp = bin_ptr.data() + (size_t)c * (m + 1);
+        std::vector<uint32_t> cnt(m + 1, 0);
         for (int j = j0; j < j1; ++j) cnt[bin[j] + 1]++;
         for (int l = 0; l < m; ++l) cnt[l + 1] += cnt[l];
-        for (int l = 0; l <= m; ++l) bp[l] = j0 + cnt[l];
-        std::vector<int32_t> cur(cnt.begin(), cnt.end() - 1);
-        for (int j = j0; j < j1; ++j) {  // ascending j inside each bin
+        for (int l = 0; l <= m; ++l) bp[l] = (uint32_t)j0 + cnt[l];
+        std::vector<uint32_t> cur(cnt.begin(), cnt.end() - 1);
+        for (int j = j0; j < j1; ++j) {  // ascending j inside each bin (deterministic summation order)
             const int k = j - j0;
-            const uint32_t off = (uint32_t)((k >> 2) * 129 + (k & 3) * 32);
-            entries[j0 + cur[bin[j]]++] = off | (sgn[j] < 0 ? 0x80000000u : 0u);
+            entries[j0 + cur[bin[j]]++] = (uint16_t)((k >> 2) * 129 + (k & 3) * 32);
         }
     }
-    CK(cudaMalloc(&H->d_entries, sizeof(uint32_t) * std::max(1, d)));
-    CK(cudaMalloc(&H->d_binptr, sizeof(int32_t) * bin_ptr.size()));
-    CK(cudaMemcpy(H->d_entries, entries.data(), sizeof(uint32_t) * d, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(H->d_binptr, bin_ptr.data(), sizeof(int32_t) * bin_ptr.size(), cudaMemcpyHostToDevice));
-    H->plan = SketchPlanDev{d, m, p->L, p->K, Q, vpt, nchunks, H->d_entries, H->d_binptr};
+    CK(cudaMalloc(&H->d_entries, sizeof(uint16_t) * std::max(1, d)));
+    CK(cudaMalloc(&H->d_binptr, sizeof(uint32_t) * bin_ptr.size()));
+    CK(cudaMalloc(&H->d_signs, sizeof(uint32_t) * sign_bits.size()));
+    CK(cudaMemcpy(H->d_entries, entries.data(), sizeof(uint16_t) * d, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(H->d_binptr, bin_ptr.data(), sizeof(uint32_t) * bin_ptr.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(H->d_signs, sign_bits.data(), sizeof(uint32_t) * sign_bits.size(), cudaMemcpyHostToDevice));
+    int max_cnt = 0;
+    for (int c = 0; c < nchunks; ++c)
+        for (int l = 0; l < m; ++l)
+            max_cnt = std::max(max_cnt, (int)(bin_ptr[(size_t)c * (m + 1) + l + 1] - bin_ptr[(size_t)c * (m + 1) + l]));
+    H->plan = SketchPlanDev{d, m, p->L, p->K, Q, vpt, nchunks, max_cnt, H->d_entries, H->d_binptr, H->d_signs};
     return LSH_OK;
 }
 
@@ -326,6 +324,7 @@ static void free_handle(lsh_handle* H) {
     if (!H) return;
     cudaFree(H->d_entries);
     cudaFree(H->d_binptr);
+    cudaFree(H->d_signs);
     cudaFree(H->d_coff);
     cudaFree(H->d_R);
     cudaFree(H->d_flags);

@@ -187,6 +187,36 @@ __global__ void segsort_small(uint64_t* __restrict__ keys, uint32_t* __restrict_
     }
 }
 
+// Sorting network with ascending comparators only (bitonic sort with a "flip" first
+// merge step), so indices >= len behave as +infinity and need no padding.
+template <typename KeyAt, typename Swap>
+__device__ void ascending_network(int64_t len, KeyAt less_at, Swap swap_at, bool smem) {
+    int64_t P = 1;
+    while (P < len) P <<= 1;
+    for (int64_t size = 2; size <= P; size <<= 1) {
+        for (int64_t stride = size >> 1; stride > 0; stride >>= 1) {
+            const bool flip = (stride == (size >> 1));
+            for (int64_t i = threadIdx.x; i < (P >> 1); i += blockDim.x) {
+                int64_t a, b;
+                if (flip) {
+                    const int64_t blk = i / stride, j = i % stride;
+                    a = blk * size + j;
+                    b = blk * size + size - 1 - j;
+                } else {
+                    a = (i / stride) * 2 * stride + (i % stride);
+                    b = a + stride;
+                }
+                if (b < len && less_at(b, a)) swap_at(a, b);
+            }
+            if (smem) __syncthreads();
+            else {
+                __threadfence_block();
+                __syncthreads();
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(1024) segsort_big(uint64_t* __restrict__ keys, uint32_t* __restrict__ ids, int64_t n,
                                                     const uint32_t* overflow, int cap, int* flags) {
     extern __shared__ __align__(16) unsigned char sm[];
@@ -197,56 +227,35 @@ __global__ void __launch_bounds__(1024) segsort_big(uint64_t* __restrict__ keys,
     for (uint32_t e = blockIdx.x; e < count; e += gridDim.x) {
         const int t = overflow[1 + 3 * e];
         const int64_t lo = overflow[2 + 3 * e], hi = overflow[3 + 3 * e];
-        uint64_t* k = keys + (int64_t)t * n;
-        uint32_t* d = ids + (int64_t)t * n;
+        uint64_t* k = keys + (int64_t)t * n + lo;
+        uint32_t* d = ids + (int64_t)t * n + lo;
         const int64_t len = hi - lo;
-        if (len > kSegBig) {
-            // Only supported when every key is equal (then already id-ascending).
-            __shared__ int neq;
-            if (threadIdx.x == 0) neq = 0;
-            __syncthreads();
-            for (int64_t a = lo + 1 + threadIdx.x; a < hi; a += blockDim.x)
-                if (k[a] != k[lo]) neq = 1;
-            __syncthreads();
-            if (neq && threadIdx.x == 0) atomicOr(flags, 4);
-            __syncthreads();
-            continue;
-        }
-        int P = 1;
-        while (P < len) P <<= 1;
-        for (int a = threadIdx.x; a < P; a += blockDim.x) {
-            if (a < len) {
-                sk[a] = k[lo + a];
-                si[a] = d[lo + a];
-            } else {
-                sk[a] = ~0ull;
-                si[a] = 0xffffffffu;
+        if (len <= kSegBig) {
+            for (int64_t a = threadIdx.x; a < len; a += blockDim.x) {
+                sk[a] = k[a];
+                si[a] = d[a];
             }
-        }
-        __syncthreads();
-        for (int size = 2; size <= P; size <<= 1) {
-            for (int stride = size >> 1; stride > 0; stride >>= 1) {
-                for (int a = threadIdx.x; a < P; a += blockDim.x) {
-                    const int b = a ^ stride;
-                    if (b > a) {
-                        const bool up = (a & size) == 0;
-                        const bool sw = up ? kless(sk[b], si[b], sk[a], si[a]) : kless(sk[a], si[a], sk[b], si[b]);
-                        if (sw) {
-                            const uint64_t tk = sk[a];
-                            sk[a] = sk[b];
-                            sk[b] = tk;
-                            const uint32_t ti = si[a];
-                            si[a] = si[b];
-                            si[b] = ti;
-                        }
-                    }
-                }
-                __syncthreads();
+            __syncthreads();
+            ascending_network(
+                len, [&](int64_t x, int64_t y) { return kless(sk[x], si[x], sk[y], si[y]); },
+                [&](int64_t x, int64_t y) {
+                    const uint64_t tk = sk[x]; sk[x] = sk[y]; sk[y] = tk;
+                    const uint32_t ti = si[x]; si[x] = si[y]; si[y] = ti;
+                },
+                true);
+            for (int64_t a = threadIdx.x; a < len; a += blockDim.x) {
+                k[a] = sk[a];
+                d[a] = si[a];
             }
-        }
-        for (int a = threadIdx.x; a < len; a += blockDim.x) {
-            k[lo + a] = sk[a];
-            d[lo + a] = si[a];
+        } else {
+            // long segment (many equal keys): the same network in place in global memory
+            ascending_network(
+                len, [&](int64_t x, int64_t y) { return kless(k[x], d[x], k[y], d[y]); },
+                [&](int64_t x, int64_t y) {
+                    const uint64_t tk = k[x]; k[x] = k[y]; k[y] = tk;
+                    const uint32_t ti = d[x]; d[x] = d[y]; d[y] = ti;
+                },
+                false);
         }
         __syncthreads();
     }

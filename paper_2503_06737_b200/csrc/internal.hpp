@@ -16,16 +16,18 @@ namespace lshb {
 // The host planner turns the per-coordinate (bin, sign) map of Def. CS
 // / Def. HCS into, per coordinate chunk and per
 // bin, the list of contributing coordinates ("entries"), sorted ascending.
-// Entry encoding: bits 0..30 = word offset of the coordinate inside the staged
-// transposed tile (k>>2)*129 + (k&3)*32, bit 31 = sign (1 = negative).
+// Entries are the word offsets (k>>2)*129 + (k&3)*32 of the coordinates inside the
+// staged transposed tile; signs are applied while staging (sign_bits).
 // ---------------------------------------------------------------------------
 struct SketchPlanDev {
     int d, m, L, K;
     int Q;            // coordinates per chunk (64 * VPT)
-    int vpt;          // float4 registers per thread (template selector)
+    int vpt;          // float4 registers per thread (template selector: 1, 4, 16)
     int nchunks;
-    const uint32_t* entries;  // d entries
-    const int32_t* bin_ptr;   // [nchunks][m+1]
+    int max_cnt;      // largest number of coordinates of one bin inside one chunk
+    const uint16_t* entries;    // d entries: word offset (k>>2)*129 + (k&3)*32 of the coordinate in its chunk
+    const uint32_t* bin_ptr;    // [nchunks][m+1] absolute entry index where each bin starts
+    const uint32_t* sign_bits;  // [ceil(d/32)] bit j set = sign(j) = -1 (applied while staging)
 };
 
 struct DiscretizeDev {
@@ -45,7 +47,7 @@ struct HashOut {
 // Launchers (return cudaError_t of the launch).
 cudaError_t launch_sketch(const SketchPlanDev& plan, const DiscretizeDev& disc, const float* X, int64_t n,
                           int64_t ld, HashOut out, int num_sms, cudaStream_t s);
-size_t sketch_smem_bytes(int Q, int m, int nchunks);
+size_t sketch_smem_bytes(int Q, int m, int d, int nchunks);
 
 cudaError_t launch_dense_gemm_f32(const float* X, int64_t n, int64_t ld, const uint16_t* Rbf16, int m, int d,
                                   float* Y, cudaStream_t s);

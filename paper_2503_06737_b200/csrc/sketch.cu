@@ -72,6 +72,29 @@ __device__ __forceinline__ int32_t floor_code(float q, int* flags) {
 
 // Discretise one bin and fold it into the running table key (shared by every
 // projection kernel so the arithmetic is identical across schemes).
+template <bool E2>
+struct KeyAccT {
+    uint64_t f;
+    __device__ __forceinline__ KeyAccT() : f(E2 ? LSHB_FNV_OFFSET : 0ull) {}
+    // q-path for E2LSH: z = floor(y * c_scale + c_off_l) (= floor((sqrt(m) y + b)/w) for
+    // power-of-two w, a single fp32 rounding); SRP: bit = [y > 0].
+    __device__ __forceinline__ int32_t add(float y, float coff, int kk, int* flags) {
+        if constexpr (E2) {
+            (void)kk;
+            const int32_t z = floor_code(y, flags);
+            f = (f ^ (uint64_t)(uint32_t)z) * LSHB_FNV_PRIME;
+            return z;
+        } else {
+            (void)coff;
+            (void)flags;
+            f |= (y > 0.0f ? 1ull : 0ull) << kk;
+            return y > 0.0f ? 1 : 0;
+        }
+    }
+    __device__ __forceinline__ uint64_t key() const { return E2 ? fmix64_dev(f) : f; }
+};
+
+// Legacy helper kept for keys_from_proj (runtime scheme flag).
 struct KeyAcc {
     uint64_t f;
     __device__ __forceinline__ void init(int e2lsh) { f = e2lsh ? LSHB_FNV_OFFSET : 0ull; }
@@ -92,24 +115,86 @@ struct KeyAcc {
     __device__ __forceinline__ uint64_t key(int e2lsh) const { return e2lsh ? fmix64_dev(f) : f; }
 };
 
-template <int VPT, bool VEC>
+// Shared-memory image of the plan (loaded once per persistent CTA).
+struct SmemPlan {
+    float* T;          // [Q4][129] transposed, sign-applied tile
+    float* ys;         // [m][32] partial bins (multi-chunk only)
+    uint32_t* bp;      // [nchunks][m+1] entry index where each bin starts
+    uint16_t* ent;     // [d] word offset of each contributing coordinate in T
+    float* coff;       // [m] b_l / w
+    uint32_t* sgn;     // [ceil(d/32)] bit j = coordinate j has sign -1
+};
+
+__host__ __device__ inline size_t sketch_smem_layout(int Q, int m, int d, int nchunks, size_t* off_ys, size_t* off_bp,
+                                                     size_t* off_ent, size_t* off_coff, size_t* off_sgn,
+                                                     size_t* off_cnt) {
+    size_t o = (size_t)(Q / 4) * 129 * 4;
+    *off_ys = o;
+    if (nchunks > 1) o += (size_t)m * 32 * 4;
+    *off_bp = o;
+    o += (size_t)nchunks * (m + 1) * 4;
+    *off_cnt = o = (o + 15) / 16 * 16;
+    o += ((size_t)nchunks * m + 15) / 16 * 16;
+    *off_ent = o;
+    o += (((size_t)(d + 2) * 2) + 15) / 16 * 16;
+    *off_coff = o;
+    o += (size_t)m * 4;
+    *off_sgn = o;
+    o += (size_t)((d + 31) / 32) * 4;
+    return o;
+}
+
+template <int VPT, bool VEC, int KT, bool E2, bool SINGLE>
 __global__ void __launch_bounds__(kThreads, 1)
     sketch_kernel(SketchPlanDev plan, DiscretizeDev dz, const float* __restrict__ X, int64_t n, int64_t ld,
-                  HashOut out) {
-    extern __shared__ __align__(16) float smem[];
+                  HashOut out, int dbg) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int Q = 64 * VPT;
     constexpr int Q4 = Q / 4;                 // float4 per row of a chunk
     constexpr int RPI = kThreads / Q4;        // rows per load iteration (VEC path)
-    float* T = smem;                          // [Q4][129] transposed tile
-    float* ys = smem + Q4 * 129;              // [m][32] partial bins (multi-chunk only)
+    const int m = plan.m, L = plan.L, d = plan.d, nch = plan.nchunks;
+    const int K = KT > 0 ? KT : plan.K;
+    size_t o_ys, o_bp, o_ent, o_coff, o_sgn, o_cnt;
+    sketch_smem_layout(Q, m, d, nch, &o_ys, &o_bp, &o_ent, &o_coff, &o_sgn, &o_cnt);
+    float* T = reinterpret_cast<float*>(smem_raw);
+    float* ys = reinterpret_cast<float*>(smem_raw + o_ys);
+    uint32_t* s_bp = reinterpret_cast<uint32_t*>(smem_raw + o_bp);
+    uint16_t* s_ent = reinterpret_cast<uint16_t*>(smem_raw + o_ent);
+    float* s_coff = reinterpret_cast<float*>(smem_raw + o_coff);
+    uint32_t* s_sgn = reinterpret_cast<uint32_t*>(smem_raw + o_sgn);
+    uint8_t* s_cnt = reinterpret_cast<uint8_t*>(smem_raw + o_cnt);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t ntiles = (n + 31) >> 5;
-    const int m = plan.m, K = plan.K, L = plan.L, d = plan.d, nch = plan.nchunks;
     int64_t tile = blockIdx.x;
     if (tile >= ntiles) return;
 
+    // plan tables -> shared memory (once per persistent CTA)
+    for (int i = tid; i < nch * (m + 1); i += kThreads) s_bp[i] = __ldg(plan.bin_ptr + i);
+    for (int i = tid; i < d + 2; i += kThreads) s_ent[i] = i < d ? __ldg(plan.entries + i) : (uint16_t)0;
+    for (int i = tid; i < nch * m; i += kThreads) {
+        const int cc = i / m, l = i % m;
+        const uint32_t cn = __ldg(plan.bin_ptr + cc * (m + 1) + l + 1) - __ldg(plan.bin_ptr + cc * (m + 1) + l);
+        s_cnt[i] = (uint8_t)(cn < 255u ? cn : 255u);
+    }
+    for (int i = tid; i < m; i += kThreads) s_coff[i] = E2 ? __ldg(dz.c_off + i) : 0.f;
+    for (int i = tid; i < (d + 31) / 32; i += kThreads) s_sgn[i] = __ldg(plan.sign_bits + i);
+    __syncthreads();
+
     float4 buf[VPT];
+    uint32_t sm0 = 0, sm1 = 0, sm2 = 0, sm3 = 0;  // sign masks of this thread's 4 columns (VEC path)
+    auto signs_for_chunk = [&](int c) {
+        if constexpr (VEC) {
+            const int k = c * Q + 4 * (tid % Q4);
+            if (k < d) {
+                const uint32_t w = s_sgn[k >> 5] >> (k & 31);  // 4 | k and 4 | 32: never straddles words
+                sm0 = (w & 1u) << 31;
+                sm1 = ((w >> 1) & 1u) << 31;
+                sm2 = ((w >> 2) & 1u) << 31;
+                sm3 = ((w >> 3) & 1u) << 31;
+            }
+        }
+    };
 
     auto load = [&](int64_t tl, int c) {
         const int k0 = c * Q;
@@ -138,19 +223,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     };
-    auto store = [&]() {
+    auto store = [&](int c) {
         if constexpr (VEC) {
             const int r0 = tid / Q4, c4 = tid % Q4;
 #pragma unroll
             for (int v = 0; v < VPT; ++v) {
                 const int r = r0 + v * RPI;
                 float* dst = T + c4 * 129 + r;
-                dst[0] = buf[v].x;
-                dst[32] = buf[v].y;
-                dst[64] = buf[v].z;
-                dst[96] = buf[v].w;
+                dst[0] = __uint_as_float(__float_as_uint(buf[v].x) ^ sm0);
+                dst[32] = __uint_as_float(__float_as_uint(buf[v].y) ^ sm1);
+                dst[64] = __uint_as_float(__float_as_uint(buf[v].z) ^ sm2);
+                dst[96] = __uint_as_float(__float_as_uint(buf[v].w) ^ sm3);
             }
         } else {
+            const int k0 = c * Q;
 #pragma unroll
             for (int v = 0; v < VPT; ++v) {
                 const float e[4] = {buf[v].x, buf[v].y, buf[v].z, buf[v].w};
@@ -158,17 +244,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int q = 0; q < 4; ++q) {
                     const int f = tid + kThreads * (4 * v + q);
                     const int r = f / Q, k = f % Q;
-                    T[(k >> 2) * 129 + (k & 3) * 32 + r] = e[q];
+                    const int kg = min(k0 + k, d - 1);
+                    const uint32_t sg = ((s_sgn[kg >> 5] >> (kg & 31)) & 1u) << 31;
+                    T[(k >> 2) * 129 + (k & 3) * 32 + r] = __uint_as_float(__float_as_uint(e[q]) ^ sg);
                 }
             }
         }
     };
 
     int c = 0;
+    signs_for_chunk(0);
     load(tile, 0);
+    const float* Tl = T + lane;
+    const float cs = dz.c_scale;
     while (true) {
         __syncthreads();  // previous gathers finished with T
-        store();
+        store(c);
         __syncthreads();
         int64_t ntile = tile;
         int nc = c + 1;
@@ -178,31 +269,82 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const bool has_next = ntile < ntiles;
         if (has_next) load(ntile, nc);  // in flight during the gathers below
+        if constexpr (!SINGLE) signs_for_chunk(nc);
 
-        const bool first = (c == 0), last = (c == nch - 1);
-        const int32_t* bp = plan.bin_ptr + (int64_t)c * (m + 1);
+        const bool first = SINGLE || c == 0, last = SINGLE || c == nch - 1;
         const int64_t row = tile * 32 + lane;
         const bool valid = row < n;
+        const uint32_t* bpc = s_bp + (SINGLE ? 0 : c * (m + 1));
+        const uint8_t* cntc = s_cnt + (SINGLE ? 0 : (size_t)c * m);
         for (int t = warp; t < L; t += kWarps) {
-            KeyAcc ka;
-            ka.init(dz.e2lsh);
-            int e = __ldg(bp + t * K);
-            for (int kk = 0; kk < K; ++kk) {
+            uint32_t e = bpc[t * K];
+            uint64_t f = E2 ? LSHB_FNV_OFFSET : 0ull;
+            uint32_t sbits = 0;
+            float qmax = 0.f, qnan = 0.f;
+            // one bin: y = sum of its (sign-applied) coordinates, ascending coordinate order
+            auto bin = [&](int kk, uint32_t cnt) {
                 const int l = t * K + kk;
-                const int e1 = __ldg(bp + l + 1);
                 float acc = first ? 0.0f : ys[l * 32 + lane];
-                for (; e < e1; ++e) {
-                    const uint32_t en = __ldg(plan.entries + e);
-                    const uint32_t v = __float_as_uint(T[(en & 0x7fffffffu) + lane]) ^ (en & 0x80000000u);
-                    acc += __uint_as_float(v);
+                const float v0 = Tl[s_ent[e]];      // s_ent is padded: always in bounds
+                const float v1 = Tl[s_ent[e + 1]];
+                if (cnt <= 2) {                      // m ~ d: 0..2 coordinates per bin, branch-free
+                    acc = cnt > 0 ? acc + v0 : acc;
+                    acc = cnt > 1 ? acc + v1 : acc;
+                } else {
+                    acc = (acc + v0) + v1;
+                    for (uint32_t j = 2; j < cnt; ++j) acc += Tl[s_ent[e + j]];
                 }
+                e += cnt;
                 if (!last) {
                     ys[l * 32 + lane] = acc;
-                } else {
-                    ka.add(acc, l, kk, row, valid, m, dz, out);
+                    return;
                 }
+                int32_t z;
+                if constexpr (E2) {
+                    const float q = fmaf(acc, cs, s_coff[l]);
+                    qmax = fmaxf(qmax, fabsf(q));
+                    qnan = fmaf(q, 0.f, qnan);      // NaN / Inf detector
+                    z = __float_as_int(__fadd_rd(q, 12582912.0f)) - 0x4B400000;  // floor(q), |q| < 2^22
+                    f = (f ^ (uint64_t)(uint32_t)z) * LSHB_FNV_PRIME;
+                } else {
+                    z = acc > 0.0f ? 1 : 0;
+                    if (KT > 0 && KT <= 32) sbits |= (uint32_t)z << kk;
+                    else f |= (uint64_t)z << kk;
+                }
+                if (KT == 0 && dbg && valid) {  // debug outputs only in the generic instantiation
+                    if (out.proj) out.proj[row * m + l] = acc;
+                    if (E2 && out.codes) out.codes[row * m + l] = z;
+                    if (!E2 && out.bits && z) atomicOr(&out.bits[row * ((m + 31) >> 5) + (l >> 5)], 1u << (l & 31));
+                }
+            };
+            if constexpr (KT > 0) {
+                uint32_t cw[KT / 4];
+                const uint32_t* cp = reinterpret_cast<const uint32_t*>(cntc + t * KT);
+#pragma unroll
+                for (int i = 0; i < KT / 4; ++i) cw[i] = cp[i];
+#pragma unroll
+                for (int kk = 0; kk < KT; ++kk) bin(kk, (cw[kk >> 2] >> (8 * (kk & 3))) & 255u);
+            } else {
+                for (int kk = 0; kk < K; ++kk) bin(kk, bpc[t * K + kk + 1] - bpc[t * K + kk]);
             }
-            if (last && valid && out.keys) out.keys[(int64_t)t * n + row] = ka.key(dz.e2lsh);
+            if (!last) continue;
+            if constexpr (E2) {
+                if (!(qmax < 4194304.0f) || qnan != 0.0f) {
+                    // rare: a code outside the fast floor range; redo this table exactly
+                    f = LSHB_FNV_OFFSET;
+                    for (int kk = 0; kk < K; ++kk) {
+                        const int l = t * K + kk;
+                        float acc = first ? 0.0f : ys[l * 32 + lane];
+                        for (uint32_t j = bpc[l]; j < bpc[l + 1]; ++j) acc += Tl[s_ent[j]];
+                        const int32_t z = floor_code(fmaf(acc, cs, s_coff[l]), dz.flags);
+                        f = (f ^ (uint64_t)(uint32_t)z) * LSHB_FNV_PRIME;
+                        if (KT == 0 && dbg && valid && out.codes) out.codes[row * m + l] = z;
+                    }
+                }
+            } else if (KT > 0 && KT <= 32) {
+                f = sbits;
+            }
+            if (valid && out.keys) out.keys[(int64_t)t * n + row] = E2 ? fmix64_dev(f) : f;
         }
         if (!has_next) break;
         tile = ntile;
@@ -210,43 +352,61 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-size_t sketch_smem_bytes(int Q, int m, int nchunks) {
-    size_t b = (size_t)(Q / 4) * 129 * sizeof(float);
-    if (nchunks > 1) b += (size_t)m * 32 * sizeof(float);
-    return b;
+size_t sketch_smem_bytes(int Q, int m, int d, int nchunks) {
+    size_t a, b, c, e, f, g;
+    return sketch_smem_layout(Q, m, d, nchunks, &a, &b, &c, &e, &f, &g);
 }
 
-template <int VPT, bool VEC>
+template <int VPT, bool VEC, int KT, bool E2, bool SINGLE>
 static cudaError_t launch_t(const SketchPlanDev& plan, const DiscretizeDev& dz, const float* X, int64_t n, int64_t ld,
                             HashOut out, int num_sms, cudaStream_t s) {
-    const size_t smem = sketch_smem_bytes(64 * VPT, plan.m, plan.nchunks);
-    cudaError_t e = cudaFuncSetAttribute(sketch_kernel<VPT, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    const size_t smem = sketch_smem_bytes(64 * VPT, plan.m, plan.d, plan.nchunks);
+    auto kern = sketch_kernel<VPT, VEC, KT, E2, SINGLE>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t ntiles = (n + 31) / 32;
     const int grid = (int)(ntiles < num_sms ? ntiles : num_sms);
-    sketch_kernel<VPT, VEC><<<grid, kThreads, smem, s>>>(plan, dz, X, n, ld, out);
+    const int dbg = (out.codes || out.bits || out.proj) ? 1 : 0;
+    kern<<<grid, kThreads, smem, s>>>(plan, dz, X, n, ld, out, dbg);
     return cudaGetLastError();
+}
+
+template <int VPT, bool VEC, bool SINGLE>
+static cudaError_t launch_k(const SketchPlanDev& plan, const DiscretizeDev& dz, const float* X, int64_t n, int64_t ld,
+                            HashOut out, int num_sms, cudaStream_t s) {
+    const bool e2 = dz.e2lsh != 0;
+    const bool dbg = out.codes || out.bits || out.proj;  // debug outputs: generic instantiation
+    if (plan.K == 16 && plan.max_cnt <= 255 && !dbg)
+        return e2 ? launch_t<VPT, VEC, 16, true, SINGLE>(plan, dz, X, n, ld, out, num_sms, s)
+                  : launch_t<VPT, VEC, 16, false, SINGLE>(plan, dz, X, n, ld, out, num_sms, s);
+    if (plan.K == 8 && plan.max_cnt <= 255 && !dbg)
+        return e2 ? launch_t<VPT, VEC, 8, true, SINGLE>(plan, dz, X, n, ld, out, num_sms, s)
+                  : launch_t<VPT, VEC, 8, false, SINGLE>(plan, dz, X, n, ld, out, num_sms, s);
+    return e2 ? launch_t<VPT, VEC, 0, true, SINGLE>(plan, dz, X, n, ld, out, num_sms, s)
+              : launch_t<VPT, VEC, 0, false, SINGLE>(plan, dz, X, n, ld, out, num_sms, s);
 }
 
 cudaError_t launch_sketch(const SketchPlanDev& plan, const DiscretizeDev& dz, const float* X, int64_t n, int64_t ld,
                           HashOut out, int num_sms, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     const bool vec = (plan.d % 4 == 0) && (ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
-#define LSHB_CASE(V)                                                                   \
-    case V:                                                                            \
-        return vec ? launch_t<V, true>(plan, dz, X, n, ld, out, num_sms, s)           \
-                   : launch_t<V, false>(plan, dz, X, n, ld, out, num_sms, s);
+    const bool single = plan.nchunks == 1;
     switch (plan.vpt) {
-        LSHB_CASE(1)
-        LSHB_CASE(2)
-        LSHB_CASE(4)
-        LSHB_CASE(8)
-        LSHB_CASE(16)
+        case 1:
+            return vec ? launch_k<1, true, true>(plan, dz, X, n, ld, out, num_sms, s)
+                       : launch_k<1, false, true>(plan, dz, X, n, ld, out, num_sms, s);
+        case 4:
+            return vec ? launch_k<4, true, true>(plan, dz, X, n, ld, out, num_sms, s)
+                       : launch_k<4, false, true>(plan, dz, X, n, ld, out, num_sms, s);
+        case 16:
+            if (single)
+                return vec ? launch_k<16, true, true>(plan, dz, X, n, ld, out, num_sms, s)
+                           : launch_k<16, false, true>(plan, dz, X, n, ld, out, num_sms, s);
+            return vec ? launch_k<16, true, false>(plan, dz, X, n, ld, out, num_sms, s)
+                       : launch_k<16, false, false>(plan, dz, X, n, ld, out, num_sms, s);
         default:
             return cudaErrorInvalidValue;
     }
-#undef LSHB_CASE
 }
 
 // ---------------------------------------------------------------------------

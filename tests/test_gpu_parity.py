@@ -90,7 +90,8 @@ def test_c4_full_size_sampled(scheme):
     pr = parity.check_proj(out["proj"][torch.from_numpy(rows).cuda()].cpu().numpy(), ref["proj"],
                            parity.sigma(p, t, Xs))
     assert pr["bad"] == 0 and pr["bad_empty"] == 0, pr
-    kr = parity.check_keys(p, ref, out["keys"][:, torch.from_numpy(rows).cuda()].cpu().numpy())
+    kr = parity.check_keys(p, ref, out["keys"].view(torch.int64)[:, torch.from_numpy(rows).cuda()].cpu().numpy()
+                           .view(np.uint64))
     assert kr["mismatch_outside_exempt"] == 0, kr
 
 
