@@ -270,7 +270,6 @@ struct lsh_index {
     int L = 0;
     IndexDev dev{};
     void* mem = nullptr;
-    uint32_t* nb_host = nullptr;
     cudaEvent_t done = nullptr;
     cudaStream_t stream = nullptr;  // build stream: memory is freed stream-ordered on it
 };
@@ -289,7 +288,7 @@ static lsh_status build_plan(lsh_handle* H) {
         return LSH_OK;
     }
     std::vector<uint32_t> bin_ptr((size_t)nchunks * (m + 1), 0);
-    std::vector<uint16_t> entries(d);
+    std::vector<uint16_t> pos(d);
     std::vector<uint32_t> sign_bits((d + 31) / 32, 0);
     for (int j = 0; j < d; ++j)
         if (sgn[j] < 0) sign_bits[j >> 5] |= 1u << (j & 31);
@@ -303,13 +302,14 @@ static lsh_status build_plan(lsh_handle* H) {
         std::vector<uint32_t> cur(cnt.begin(), cnt.end() - 1);
         for (int j = j0; j < j1; ++j) {  // ascending j inside each bin (deterministic summation order)
             const int k = j - j0;
-            entries[j0 + cur[bin[j]]++] = (uint16_t)((k >> 2) * 129 + (k & 3) * 32);
+            (void)k;
+            pos[j] = (uint16_t)(cur[bin[j]]++);
         }
     }
     CK(cudaMalloc(&H->d_entries, sizeof(uint16_t) * std::max(1, d)));
     CK(cudaMalloc(&H->d_binptr, sizeof(uint32_t) * bin_ptr.size()));
     CK(cudaMalloc(&H->d_signs, sizeof(uint32_t) * sign_bits.size()));
-    CK(cudaMemcpy(H->d_entries, entries.data(), sizeof(uint16_t) * d, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(H->d_entries, pos.data(), sizeof(uint16_t) * d, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(H->d_binptr, bin_ptr.data(), sizeof(uint32_t) * bin_ptr.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(H->d_signs, sign_bits.data(), sizeof(uint32_t) * sign_bits.size(), cudaMemcpyHostToDevice));
     int max_cnt = 0;
@@ -349,6 +349,15 @@ extern "C" lsh_status lsh_create(const lsh_params* p, lsh_handle** out) {
     cudaError_t e = cudaSetDevice(p->device);
     if (e != cudaSuccess) return fail(cuda_fail(e, "cudaSetDevice"));
     cudaDeviceGetAttribute(&H->num_sms, cudaDevAttrMultiProcessorCount, p->device);
+    {
+        // Scratch and index buffers come from the device's stream-ordered pool; keep freed
+        // memory cached in the pool instead of unmapping it at every synchronisation.
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, p->device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
     draw(p, H->host, true);
     H->key_width = is_e2lsh(p->scheme) ? 64 : p->K;
     const int m = p->m;
@@ -408,7 +417,8 @@ extern "C" lsh_status lsh_check(const lsh_handle* h) {
 // ---------------------------------------------------------------------------
 // hashing
 // ---------------------------------------------------------------------------
-static lsh_status hash_impl(const lsh_handle* H, const float* X, int64_t n, int64_t ld, HashOut out, cudaStream_t s) {
+static lsh_status hash_impl(const lsh_handle* H, const float* X, int64_t n, int64_t ld, HashOut out, cudaStream_t s,
+                            const char* tname = "sketch") {
     const lsh_params& p = H->p;
     if (out.bits && !is_e2lsh(p.scheme)) {
         CK(cudaMemsetAsync(out.bits, 0, sizeof(uint32_t) * (size_t)n * ((p.m + 31) / 32), s));
@@ -433,10 +443,10 @@ static lsh_status hash_impl(const lsh_handle* H, const float* X, int64_t n, int6
         return LSH_OK;
     }
     if (!H->sketch_ok) return LSH_EUNSUPPORTED;
-    timing_begin("sketch", s);
+    timing_begin(tname, s);
     cudaError_t e = launch_sketch(H->plan, H->disc, X, n, ld, out, H->num_sms, s);
     count_launch();
-    timing_end("sketch", s);
+    timing_end(tname, s);
     if (e != cudaSuccess) return cuda_fail(e, "sketch");
     return LSH_OK;
 }
@@ -475,7 +485,6 @@ static lsh_status alloc_index(const lsh_handle* H, int64_t n, cudaStream_t s, ls
     I->dev.ids = (uint32_t*)(base + b_uk);
     I->dev.offs = (uint32_t*)(base + b_uk + b_ids);
     I->dev.nb = (uint32_t*)(base + b_uk + b_ids + b_off);
-    cudaMallocHost(&I->nb_host, b_nb);
     cudaEventCreateWithFlags(&I->done, cudaEventDisableTiming);
     *out = I;
     return LSH_OK;
@@ -513,7 +522,6 @@ static lsh_status group_impl(const lsh_handle* H, const uint64_t* keys, uint64_t
     cudaError_t e = launch_group(keys, n, L, (uint32_t)id_base, H->key_width, sc, I->dev, H->d_flags, s);
     if (e != cudaSuccess) return cuda_fail(e, "group");
     if (mem) CK(cudaFreeAsync(mem, s));
-    CK(cudaMemcpyAsync(I->nb_host, I->dev.nb, sizeof(uint32_t) * L, cudaMemcpyDeviceToHost, s));
     CK(cudaEventRecord(I->done, s));
     return LSH_OK;
 }
@@ -570,11 +578,13 @@ extern "C" lsh_status lsh_index_view(const lsh_index* idx, int32_t t, const uint
     if (!idx) return LSH_ESTATE;
     if (t < 0 || t >= idx->L) return LSH_EDIM;
     CK(cudaEventSynchronize(idx->done));
+    uint32_t nbv = 0;
+    CK(cudaMemcpy(&nbv, idx->dev.nb + t, sizeof(uint32_t), cudaMemcpyDeviceToHost));
     const int64_t n = idx->n;
     if (ids) *ids = idx->dev.ids + (int64_t)t * n;
     if (ukeys) *ukeys = idx->dev.ukeys + (int64_t)t * n;
     if (offs) *offs = idx->dev.offs + (int64_t)t * (n + 1);
-    if (nb) *nb = idx->nb_host[t];
+    if (nb) *nb = nbv;
     return LSH_OK;
 }
 
@@ -584,7 +594,6 @@ extern "C" void lsh_index_destroy(lsh_index* idx) {
     if (!idx) return;
     if (idx->done) cudaEventSynchronize(idx->done);
     if (idx->mem) cudaFreeAsync(idx->mem, idx->stream);
-    if (idx->nb_host) cudaFreeHost(idx->nb_host);
     if (idx->done) cudaEventDestroy(idx->done);
     delete idx;
 }
@@ -599,7 +608,7 @@ extern "C" lsh_status lsh_query_buckets(const lsh_handle* h, const lsh_index* id
     cudaStream_t s = (cudaStream_t)stream;
     uint64_t* qk = nullptr;
     CK(cudaMallocAsync((void**)&qk, sizeof(uint64_t) * (size_t)h->p.L * nq, s));
-    lsh_status st = hash_impl(h, Q, nq, ld, HashOut{qk, nullptr, nullptr, nullptr}, s);
+    lsh_status st = hash_impl(h, Q, nq, ld, HashOut{qk, nullptr, nullptr, nullptr}, s, "sketch_query");
     if (st == LSH_OK) {
         timing_begin("lookup", s);
         cudaError_t e = launch_lookup(qk, nq, h->p.L, idx->n, idx->dev, begin, end, s);

@@ -20,11 +20,12 @@
 
 namespace lshb {
 
-constexpr int kTile = 2048;        // items per radix tile
+constexpr int kTile = 4096;        // items per radix tile
 constexpr int kRT = 256;           // threads per radix block
 constexpr int kRounds = kTile / kRT;
-constexpr int kSegSmall = 64;      // segments up to this size: in-place insertion sort
-constexpr int kSegBig = 8192;      // CTA bitonic capacity
+constexpr int kSegWin = 2048;      // positions owned by one segment-sort block
+constexpr int kSegCap = 256;       // longest segment sorted by the windowed kernel
+constexpr int kSegBig = 8192;      // CTA bitonic capacity in shared memory
 
 size_t group_tiles(int64_t n) { return (size_t)((n + kTile - 1) / kTile); }
 
@@ -94,54 +95,98 @@ __global__ void __launch_bounds__(1024) scan_rows(uint32_t* a, int64_t len, int6
     }
 }
 
+// Stable scatter of one 4096-item tile by an 8-bit digit.  Warp w owns the tile's
+// items [512w, 512w+512) (coalesced 32-item rounds); a warp ranks its items with
+// match_any against its own running per-digit counters (no block barrier per
+// round), then one block-wide pass turns (digit, warp) counts into offsets.  Items
+// are placed in digit order in shared memory and written out so that consecutive
+// threads write consecutive addresses.  Order inside a digit = item order: stable.
 template <bool IMPLICIT_IDS>
 __global__ void __launch_bounds__(kRT) radix_downsweep(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ iin,
                                                        uint64_t* __restrict__ kout, uint32_t* __restrict__ iout,
                                                        int64_t n, int sh, const uint32_t* __restrict__ hist, int T,
                                                        uint32_t id_base) {
-    __shared__ uint32_t wcount[kRT / 32][256];
-    __shared__ uint32_t woff[kRT / 32][256];
-    __shared__ uint32_t run_base[256];
+    constexpr int W = kRT / 32;             // warps
+    constexpr int PER_WARP = kTile / W;     // 512 items
+    constexpr int R = PER_WARP / 32;        // 16 rounds
+    __shared__ uint32_t wrun[W][256];       // per-warp running digit counts, then warp offsets
     __shared__ uint32_t tile_off[256];
+    __shared__ uint32_t local_off[256];
+    __shared__ uint32_t ws[W];
+    extern __shared__ __align__(16) unsigned char dsm[];
+    uint64_t* sk = reinterpret_cast<uint64_t*>(dsm);                  // [kTile]
+    uint32_t* si = reinterpret_cast<uint32_t*>(dsm + kTile * 8);      // [kTile]
     const int t = blockIdx.y, tile = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int w = 0; w < kRT / 32; ++w) wcount[w][threadIdx.x] = 0;
-    run_base[threadIdx.x] = 0;
+    for (int w = 0; w < W; ++w) wrun[w][threadIdx.x] = 0;
     tile_off[threadIdx.x] = hist[((int64_t)t * 256 + threadIdx.x) * T + tile];
     __syncthreads();
     const int64_t tb = (int64_t)t * n;
-    for (int r = 0; r < kRounds; ++r) {
-        const int64_t i = (int64_t)tile * kTile + r * kRT + threadIdx.x;
+    const int64_t base = (int64_t)tile * kTile + warp * PER_WARP;
+    uint64_t key[R];
+    uint32_t id[R], slot[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t i = base + r * 32 + lane;
         const bool valid = i < n;
-        uint64_t key = 0;
-        uint32_t id = 0;
-        uint32_t dg = 256;
-        if (valid) {
-            key = kin[tb + i];
-            id = IMPLICIT_IDS ? id_base + (uint32_t)i : iin[tb + i];
-            dg = (uint32_t)(key >> sh) & 255u;
-        }
+        key[r] = valid ? kin[tb + i] : ~0ull;
+        id[r] = valid ? (IMPLICIT_IDS ? id_base + (uint32_t)i : iin[tb + i]) : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t i = base + r * 32 + lane;
+        const bool valid = i < n;
+        const uint32_t dg = valid ? ((uint32_t)(key[r] >> sh) & 255u) : 256u;
         const uint32_t peers = __match_any_sync(0xffffffffu, dg);
         const uint32_t rank = __popc(peers & lanemask_lt());
-        if (valid && rank == 0) wcount[warp][dg] = __popc(peers);
-        __syncthreads();
-        {
-            const int dd = threadIdx.x;
-            uint32_t acc = run_base[dd];
+        uint32_t before = 0;
+        if (valid) before = wrun[warp][dg];
+        __syncwarp();
+        if (valid && rank == 0) wrun[warp][dg] = before + __popc(peers);
+        __syncwarp();
+        slot[r] = valid ? (dg << 16) | (before + rank) : 0xffffffffu;
+    }
+    __syncthreads();
+    {   // per digit: exclusive prefix over warps, and the tile's digit totals
+        const int dd = threadIdx.x;
+        uint32_t acc = 0;
 #pragma unroll
-            for (int w = 0; w < kRT / 32; ++w) {
-                woff[w][dd] = acc;
-                acc += wcount[w][dd];
-                wcount[w][dd] = 0;
-            }
-            run_base[dd] = acc;
+        for (int w = 0; w < W; ++w) {
+            const uint32_t c = wrun[w][dd];
+            wrun[w][dd] = acc;
+            acc += c;
         }
+        // exclusive scan of totals across digits -> local_off
+        uint32_t x = acc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) ws[warp] = x;
         __syncthreads();
-        if (valid) {
-            const uint32_t pos = tile_off[dg] + woff[warp][dg] + rank;
-            kout[tb + pos] = key;
-            iout[tb + pos] = id;
+        uint32_t pre = 0;
+        for (int w = 0; w < warp; ++w) pre += ws[w];
+        local_off[dd] = pre + x - acc;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        if (slot[r] != 0xffffffffu) {
+            const uint32_t dg = slot[r] >> 16;
+            const uint32_t p = local_off[dg] + wrun[warp][dg] + (slot[r] & 0xffffu);
+            sk[p] = key[r];
+            si[p] = id[r];
         }
+    }
+    __syncthreads();
+    const int64_t cnt = min((int64_t)kTile, n - (int64_t)tile * kTile);
+    for (int p = threadIdx.x; p < cnt; p += kRT) {
+        const uint64_t k = sk[p];
+        const uint32_t dg = (uint32_t)(k >> sh) & 255u;
+        const uint32_t pos = tile_off[dg] + (p - local_off[dg]);
+        kout[tb + pos] = k;
+        iout[tb + pos] = si[p];
     }
 }
 
@@ -149,41 +194,105 @@ __device__ __forceinline__ bool kless(uint64_t ka, uint32_t ia, uint64_t kb, uin
     return ka < kb || (ka == kb && ia < ib);
 }
 
-// Segments of equal top-16 significant bits: stable sort by the full key.
-__global__ void segsort_small(uint64_t* __restrict__ keys, uint32_t* __restrict__ ids, int64_t n, int L, int pre_sh,
-                              uint32_t* overflow, int cap) {
-    const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gi >= (int64_t)L * n) return;
-    const int t = (int)(gi / n);
-    const int64_t i = gi % n;
+// Segments of equal top-16 significant bits: stable sort by the full key.  One
+// block owns the segments whose head lies in its window of kSegWin positions and
+// loads the window plus kSegCap positions of look-ahead into shared memory.
+// Segment heads are found with one block scan; each item's rank inside its
+// segment is #{smaller keys} + #{equal keys before it} (items arrive id-ascending
+// inside a segment, so this is the stable order).  Longer segments go to the
+// overflow list (segsort_big).
+__global__ void __launch_bounds__(256) segsort_window(uint64_t* __restrict__ keys, uint32_t* __restrict__ ids, int64_t n,
+                                                      int pre_sh, uint32_t* overflow, int cap) {
+    constexpr int LEN = kSegWin + kSegCap;
+    constexpr int PER = (LEN + 255) / 256;
+    __shared__ uint64_t sk[LEN];
+    __shared__ uint32_t si[LEN];
+    __shared__ uint16_t seg_of[LEN];
+    __shared__ uint16_t seg_start[LEN + 1];
+    __shared__ uint32_t ws[8];
+    __shared__ int nseg_s;
+    const int t = blockIdx.y;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t w0 = (int64_t)blockIdx.x * kSegWin;
     uint64_t* k = keys + (int64_t)t * n;
     uint32_t* d = ids + (int64_t)t * n;
-    const uint64_t pre = k[i] >> pre_sh;
-    if (i > 0 && (k[i - 1] >> pre_sh) == pre) return;  // not a segment head
-    int64_t j = i + 1;
-    while (j < n && (k[j] >> pre_sh) == pre && j - i <= kSegSmall) ++j;
-    if (j - i > kSegSmall) {
-        while (j < n && (k[j] >> pre_sh) == pre) ++j;
-        const uint32_t slot = atomicAdd(overflow, 1u);
-        if ((int)slot < cap) {
-            overflow[1 + 3 * slot] = (uint32_t)t;
-            overflow[2 + 3 * slot] = (uint32_t)i;
-            overflow[3 + 3 * slot] = (uint32_t)j;
-        }
-        return;
+    const int len = (int)min((int64_t)LEN, n - w0);
+    const int own = (int)min((int64_t)kSegWin, n - w0);
+    for (int a = threadIdx.x; a < len; a += blockDim.x) {
+        sk[a] = k[w0 + a];
+        si[a] = d[w0 + a];
     }
-    // insertion sort (stable: only strictly larger keys move right)
-    for (int64_t a = i + 1; a < j; ++a) {
-        const uint64_t kv = k[a];
-        const uint32_t iv = d[a];
-        int64_t b = a - 1;
-        while (b >= i && k[b] > kv) {
-            k[b + 1] = k[b];
-            d[b + 1] = d[b];
-            --b;
+    const uint64_t prev_pre = w0 > 0 ? (k[w0 - 1] >> pre_sh) : ~0ull;
+    __syncthreads();
+    // head flags over my PER consecutive positions, block scan -> segment ids
+    const int a0 = threadIdx.x * PER;
+    uint32_t flags = 0, cntf = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int a = a0 + q;
+        if (a < len) {
+            const uint64_t pr = a == 0 ? prev_pre : (sk[a - 1] >> pre_sh);
+            if ((sk[a] >> pre_sh) != pr) {
+                flags |= 1u << q;
+                ++cntf;
+            }
         }
-        k[b + 1] = kv;
-        d[b + 1] = iv;
+    }
+    uint32_t x = cntf;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) ws[warp] = x;
+    __syncthreads();
+    uint32_t sid = 0;
+    for (int w = 0; w < warp; ++w) sid += ws[w];
+    sid += x - cntf;  // heads before my first position
+    if (threadIdx.x == 255) nseg_s = (int)(sid + cntf);
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int a = a0 + q;
+        if (a < len) {
+            if (flags >> q & 1u) {
+                seg_start[sid] = (uint16_t)a;
+                ++sid;
+            }
+            seg_of[a] = (uint16_t)(sid == 0 ? 0xffffu : sid - 1);  // 0xffff: previous window's segment
+        }
+    }
+    __syncthreads();
+    const int nseg = nseg_s;
+    for (int li = threadIdx.x; li < len; li += blockDim.x) {
+        const uint32_t sg = seg_of[li];
+        if (sg == 0xffffu) continue;
+        const int h = seg_start[sg];
+        if (h >= own) continue;                              // head in the next window
+        const int e = (int)sg + 1 < nseg ? seg_start[sg + 1] : len;
+        const uint64_t pre = sk[li] >> pre_sh;
+        const bool beyond = (e == len) && (w0 + len < n) && (k[w0 + len] >> pre_sh) == pre;
+        if (beyond || e - h > kSegCap) {
+            if (li == h) {                                   // the head reports the long segment once
+                int64_t ge = w0 + e;
+                while (ge < n && (k[ge] >> pre_sh) == pre) ++ge;
+                const uint32_t slot = atomicAdd(overflow, 1u);
+                if ((int)slot < cap) {
+                    overflow[1 + 3 * slot] = (uint32_t)t;
+                    overflow[2 + 3 * slot] = (uint32_t)(w0 + h);
+                    overflow[3 + 3 * slot] = (uint32_t)ge;
+                }
+            }
+            continue;
+        }
+        if (e - h == 1) continue;
+        const uint64_t kv = sk[li];
+        int rank = 0;
+        for (int j = h; j < e; ++j) {
+            const uint64_t kj = sk[j];
+            rank += (kj < kv || (kj == kv && j < li)) ? 1 : 0;
+        }
+        k[w0 + h + rank] = kv;
+        d[w0 + h + rank] = si[li];
     }
 }
 
@@ -361,10 +470,14 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
         count_launch();
         timing_end("radix_scan", s);
         timing_begin("radix_downsweep", s);
-        if (p == 0)
-            radix_downsweep<true><<<g2, kRT, 0, s>>>(kin, iin, kout, iout, n, shifts[p], sc.hist, T, id_base);
-        else
-            radix_downsweep<false><<<g2, kRT, 0, s>>>(kin, iin, kout, iout, n, shifts[p], sc.hist, T, id_base);
+        const int dsm = kTile * 12;
+        if (p == 0) {
+            cudaFuncSetAttribute(radix_downsweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm);
+            radix_downsweep<true><<<g2, kRT, dsm, s>>>(kin, iin, kout, iout, n, shifts[p], sc.hist, T, id_base);
+        } else {
+            cudaFuncSetAttribute(radix_downsweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm);
+            radix_downsweep<false><<<g2, kRT, dsm, s>>>(kin, iin, kout, iout, n, shifts[p], sc.hist, T, id_base);
+        }
         count_launch();
         timing_end("radix_downsweep", s);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -376,9 +489,8 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
         timing_begin("segsort", s);
         e = cudaMemsetAsync(sc.overflow, 0, sizeof(uint32_t), s);
         if (e != cudaSuccess) return e;
-        const int64_t tot = (int64_t)L * n;
-        segsort_small<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(sorted, out.ids, n, L, W - 16, sc.overflow,
-                                                                   sc.overflow_cap);
+        const dim3 gw((unsigned)((n + kSegWin - 1) / kSegWin), L);
+        segsort_window<<<gw, 256, 0, s>>>(sorted, out.ids, n, W - 16, sc.overflow, sc.overflow_cap);
         count_launch();
         const size_t smem = kSegBig * (sizeof(uint64_t) + sizeof(uint32_t));
         cudaFuncSetAttribute(segsort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

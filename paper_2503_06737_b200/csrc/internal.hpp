@@ -15,9 +15,8 @@ namespace lshb {
 // Sparse one-nonzero-per-column projection (CS and HCS), DESIGN.md §K1.
 // The host planner turns the per-coordinate (bin, sign) map of Def. CS
 // / Def. HCS into, per coordinate chunk and per
-// bin, the list of contributing coordinates ("entries"), sorted ascending.
-// Entries are the word offsets (k>>2)*129 + (k&3)*32 of the coordinates inside the
-// staged transposed tile; signs are applied while staging (sign_bits).
+// bin, the run of contributing coordinates: coordinates are staged in bin-sorted
+// order (ascending coordinate inside a bin) with their sign already applied.
 // ---------------------------------------------------------------------------
 struct SketchPlanDev {
     int d, m, L, K;
@@ -25,8 +24,8 @@ struct SketchPlanDev {
     int vpt;          // float4 registers per thread (template selector: 1, 4, 16)
     int nchunks;
     int max_cnt;      // largest number of coordinates of one bin inside one chunk
-    const uint16_t* entries;    // d entries: word offset (k>>2)*129 + (k&3)*32 of the coordinate in its chunk
-    const uint32_t* bin_ptr;    // [nchunks][m+1] absolute entry index where each bin starts
+    const uint16_t* pos;        // [d] rank of coordinate j in its chunk's bin-sorted order (ascending j in a bin)
+    const uint32_t* bin_ptr;    // [nchunks][m+1] absolute index (chunk start + rank) where each bin starts
     const uint32_t* sign_bits;  // [ceil(d/32)] bit j set = sign(j) = -1 (applied while staging)
 };
 

@@ -115,33 +115,41 @@ struct KeyAcc {
     __device__ __forceinline__ uint64_t key(int e2lsh) const { return e2lsh ? fmix64_dev(f) : f; }
 };
 
-// Shared-memory image of the plan (loaded once per persistent CTA).
-struct SmemPlan {
-    float* T;          // [Q4][129] transposed, sign-applied tile
-    float* ys;         // [m][32] partial bins (multi-chunk only)
-    uint32_t* bp;      // [nchunks][m+1] entry index where each bin starts
-    uint16_t* ent;     // [d] word offset of each contributing coordinate in T
-    float* coff;       // [m] b_l / w
-    uint32_t* sgn;     // [ceil(d/32)] bit j = coordinate j has sign -1
-};
-
-__host__ __device__ inline size_t sketch_smem_layout(int Q, int m, int d, int nchunks, size_t* off_ys, size_t* off_bp,
-                                                     size_t* off_ent, size_t* off_coff, size_t* off_sgn,
-                                                     size_t* off_cnt) {
-    size_t o = (size_t)(Q / 4) * 129 * 4;
-    *off_ys = o;
+// Shared-memory layout of the kernel (plan tables are loaded once per persistent CTA):
+//   T    [(Q+2) x 33] fp32  staged chunk of 32 points: coordinate k of point r lives at
+//                           word pos(k)*33 + r, pos = rank of k in bin-sorted order, value
+//                           already multiplied by sign(k); so every bin is a run of
+//                           consecutive positions and lane r reads word p*33 + r
+//                           (bank-conflict free).  +2 positions: branch-free over-read.
+//   ys   [m x 32]  fp32     partial bins across chunks (multi-chunk plans only)
+//   bp   [nchunks x (m+1)]  first position (absolute coordinate index) of every bin
+//   cnt  [nchunks x m] u8   coordinates per bin per chunk (saturated at 255)
+//   pos  [d] u16            bin-sorted position of coordinate j inside its chunk
+//   coff [m] fp32           b_l / w
+//   sgn  [ceil(d/32)] u32   bit j set: sign(j) = -1
+__host__ __device__ inline size_t sketch_smem_layout(int Q, int m, int d, int nchunks, size_t* o_ys, size_t* o_bp,
+                                                     size_t* o_cnt, size_t* o_pos, size_t* o_coff, size_t* o_sgn) {
+    size_t o = (size_t)(Q + 2) * 33 * 4;
+    *o_ys = o;
     if (nchunks > 1) o += (size_t)m * 32 * 4;
-    *off_bp = o;
+    *o_bp = o;
     o += (size_t)nchunks * (m + 1) * 4;
-    *off_cnt = o = (o + 15) / 16 * 16;
+    *o_cnt = o = (o + 15) / 16 * 16;
     o += ((size_t)nchunks * m + 15) / 16 * 16;
-    *off_ent = o;
-    o += (((size_t)(d + 2) * 2) + 15) / 16 * 16;
-    *off_coff = o;
+    *o_pos = o;
+    o += ((size_t)d * 2 + 15) / 16 * 16;
+    *o_coff = o;
     o += (size_t)m * 4;
-    *off_sgn = o;
+    *o_sgn = o;
     o += (size_t)((d + 31) / 32) * 4;
     return o;
+}
+
+// max.NaN: propagates NaN so one instruction checks both range and NaN/Inf.
+__device__ __forceinline__ float fmax_nan_abs(float a, float q) {
+    float r;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(fabsf(q)));
+    return r;
 }
 
 template <int VPT, bool VEC, int KT, bool E2, bool SINGLE>
@@ -154,44 +162,48 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int RPI = kThreads / Q4;        // rows per load iteration (VEC path)
     const int m = plan.m, L = plan.L, d = plan.d, nch = plan.nchunks;
     const int K = KT > 0 ? KT : plan.K;
-    size_t o_ys, o_bp, o_ent, o_coff, o_sgn, o_cnt;
-    sketch_smem_layout(Q, m, d, nch, &o_ys, &o_bp, &o_ent, &o_coff, &o_sgn, &o_cnt);
+    size_t o_ys, o_bp, o_cnt, o_pos, o_coff, o_sgn;
+    sketch_smem_layout(Q, m, d, nch, &o_ys, &o_bp, &o_cnt, &o_pos, &o_coff, &o_sgn);
     float* T = reinterpret_cast<float*>(smem_raw);
     float* ys = reinterpret_cast<float*>(smem_raw + o_ys);
     uint32_t* s_bp = reinterpret_cast<uint32_t*>(smem_raw + o_bp);
-    uint16_t* s_ent = reinterpret_cast<uint16_t*>(smem_raw + o_ent);
+    uint8_t* s_cnt = reinterpret_cast<uint8_t*>(smem_raw + o_cnt);
+    uint16_t* s_pos = reinterpret_cast<uint16_t*>(smem_raw + o_pos);
     float* s_coff = reinterpret_cast<float*>(smem_raw + o_coff);
     uint32_t* s_sgn = reinterpret_cast<uint32_t*>(smem_raw + o_sgn);
-    uint8_t* s_cnt = reinterpret_cast<uint8_t*>(smem_raw + o_cnt);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t ntiles = (n + 31) >> 5;
     int64_t tile = blockIdx.x;
     if (tile >= ntiles) return;
 
-    // plan tables -> shared memory (once per persistent CTA)
     for (int i = tid; i < nch * (m + 1); i += kThreads) s_bp[i] = __ldg(plan.bin_ptr + i);
-    for (int i = tid; i < d + 2; i += kThreads) s_ent[i] = i < d ? __ldg(plan.entries + i) : (uint16_t)0;
     for (int i = tid; i < nch * m; i += kThreads) {
         const int cc = i / m, l = i % m;
         const uint32_t cn = __ldg(plan.bin_ptr + cc * (m + 1) + l + 1) - __ldg(plan.bin_ptr + cc * (m + 1) + l);
         s_cnt[i] = (uint8_t)(cn < 255u ? cn : 255u);
     }
+    for (int i = tid; i < d; i += kThreads) s_pos[i] = __ldg(plan.pos + i);
     for (int i = tid; i < m; i += kThreads) s_coff[i] = E2 ? __ldg(dz.c_off + i) : 0.f;
     for (int i = tid; i < (d + 31) / 32; i += kThreads) s_sgn[i] = __ldg(plan.sign_bits + i);
+    for (int i = tid; i < 2 * 33; i += kThreads) T[Q * 33 + i] = 0.f;
     __syncthreads();
 
     float4 buf[VPT];
-    uint32_t sm0 = 0, sm1 = 0, sm2 = 0, sm3 = 0;  // sign masks of this thread's 4 columns (VEC path)
-    auto signs_for_chunk = [&](int c) {
+    // staging targets of this thread's 4 columns (VEC path): word offset pos*33, sign mask
+    uint32_t so[4] = {0, 0, 0, 0}, sm[4] = {0, 0, 0, 0};
+    bool col_ok = false;
+    auto columns_for_chunk = [&](int c) {
         if constexpr (VEC) {
             const int k = c * Q + 4 * (tid % Q4);
-            if (k < d) {
-                const uint32_t w = s_sgn[k >> 5] >> (k & 31);  // 4 | k and 4 | 32: never straddles words
-                sm0 = (w & 1u) << 31;
-                sm1 = ((w >> 1) & 1u) << 31;
-                sm2 = ((w >> 2) & 1u) << 31;
-                sm3 = ((w >> 3) & 1u) << 31;
+            col_ok = k < d;
+            if (col_ok) {
+                const uint32_t w = s_sgn[k >> 5] >> (k & 31);  // 4 | k: never straddles a word
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    so[e] = (uint32_t)s_pos[k + e] * 33u;
+                    sm[e] = ((w >> e) & 1u) << 31;
+                }
             }
         }
     };
@@ -201,12 +213,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int Qc = min(Q, d - k0);
         if constexpr (VEC) {
             const int r0 = tid / Q4, c4 = tid % Q4;
+            if (4 * c4 < Qc) {
+                const float* src = X + (tl * 32 + r0) * ld + k0 + 4 * c4;
+                const int64_t stride = (int64_t)RPI * ld;
+                if (tl * 32 + 32 <= n) {  // full tile: no row predicates
 #pragma unroll
-            for (int v = 0; v < VPT; ++v) {
-                const int r = r0 + v * RPI;
-                const int64_t row = tl * 32 + r;
-                if (row < n && 4 * c4 < Qc) buf[v] = ldg_stream_f4(X + row * ld + k0 + 4 * c4);
-                else buf[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    for (int v = 0; v < VPT; ++v) buf[v] = ldg_stream_f4(src + v * stride);
+                } else {
+                    const int64_t rows_left = n - tl * 32 - r0;
+#pragma unroll
+                    for (int v = 0; v < VPT; ++v)
+                        buf[v] = v * RPI < rows_left ? ldg_stream_f4(src + v * stride) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
             }
         } else {
 #pragma unroll
@@ -225,18 +243,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     auto store = [&](int c) {
         if constexpr (VEC) {
-            const int r0 = tid / Q4, c4 = tid % Q4;
+            if (col_ok) {
+                const int r0 = tid / Q4;
 #pragma unroll
-            for (int v = 0; v < VPT; ++v) {
-                const int r = r0 + v * RPI;
-                float* dst = T + c4 * 129 + r;
-                dst[0] = __uint_as_float(__float_as_uint(buf[v].x) ^ sm0);
-                dst[32] = __uint_as_float(__float_as_uint(buf[v].y) ^ sm1);
-                dst[64] = __uint_as_float(__float_as_uint(buf[v].z) ^ sm2);
-                dst[96] = __uint_as_float(__float_as_uint(buf[v].w) ^ sm3);
+                for (int v = 0; v < VPT; ++v) {
+                    const int r = r0 + v * RPI;
+                    T[so[0] + r] = __uint_as_float(__float_as_uint(buf[v].x) ^ sm[0]);
+                    T[so[1] + r] = __uint_as_float(__float_as_uint(buf[v].y) ^ sm[1]);
+                    T[so[2] + r] = __uint_as_float(__float_as_uint(buf[v].z) ^ sm[2]);
+                    T[so[3] + r] = __uint_as_float(__float_as_uint(buf[v].w) ^ sm[3]);
+                }
             }
         } else {
             const int k0 = c * Q;
+            const int Qc = min(Q, d - k0);
 #pragma unroll
             for (int v = 0; v < VPT; ++v) {
                 const float e[4] = {buf[v].x, buf[v].y, buf[v].z, buf[v].w};
@@ -244,18 +264,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int q = 0; q < 4; ++q) {
                     const int f = tid + kThreads * (4 * v + q);
                     const int r = f / Q, k = f % Q;
-                    const int kg = min(k0 + k, d - 1);
-                    const uint32_t sg = ((s_sgn[kg >> 5] >> (kg & 31)) & 1u) << 31;
-                    T[(k >> 2) * 129 + (k & 3) * 32 + r] = __uint_as_float(__float_as_uint(e[q]) ^ sg);
+                    if (k < Qc) {
+                        const int kg = k0 + k;
+                        const uint32_t sg = ((s_sgn[kg >> 5] >> (kg & 31)) & 1u) << 31;
+                        T[(uint32_t)s_pos[kg] * 33u + r] = __uint_as_float(__float_as_uint(e[q]) ^ sg);
+                    }
                 }
             }
         }
     };
 
     int c = 0;
-    signs_for_chunk(0);
+    columns_for_chunk(0);
     load(tile, 0);
-    const float* Tl = T + lane;
     const float cs = dz.c_scale;
     while (true) {
         __syncthreads();  // previous gathers finished with T
@@ -269,32 +290,33 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const bool has_next = ntile < ntiles;
         if (has_next) load(ntile, nc);  // in flight during the gathers below
-        if constexpr (!SINGLE) signs_for_chunk(nc);
+        if constexpr (!SINGLE) columns_for_chunk(nc);
 
         const bool first = SINGLE || c == 0, last = SINGLE || c == nch - 1;
         const int64_t row = tile * 32 + lane;
         const bool valid = row < n;
         const uint32_t* bpc = s_bp + (SINGLE ? 0 : c * (m + 1));
         const uint8_t* cntc = s_cnt + (SINGLE ? 0 : (size_t)c * m);
+        const uint32_t cbase = SINGLE ? 0u : (uint32_t)(c * Q);
         for (int t = warp; t < L; t += kWarps) {
-            uint32_t e = bpc[t * K];
+            const float* p = T + (bpc[t * K] - cbase) * 33 + lane;
             uint64_t f = E2 ? LSHB_FNV_OFFSET : 0ull;
             uint32_t sbits = 0;
-            float qmax = 0.f, qnan = 0.f;
-            // one bin: y = sum of its (sign-applied) coordinates, ascending coordinate order
+            float qmax = 0.f;
+            // one bin: y = sum of its (sign-applied) coordinates in ascending coordinate order
             auto bin = [&](int kk, uint32_t cnt) {
                 const int l = t * K + kk;
                 float acc = first ? 0.0f : ys[l * 32 + lane];
-                const float v0 = Tl[s_ent[e]];      // s_ent is padded: always in bounds
-                const float v1 = Tl[s_ent[e + 1]];
+                const float v0 = p[0];
+                const float v1 = p[33];
                 if (cnt <= 2) {                      // m ~ d: 0..2 coordinates per bin, branch-free
                     acc = cnt > 0 ? acc + v0 : acc;
                     acc = cnt > 1 ? acc + v1 : acc;
                 } else {
                     acc = (acc + v0) + v1;
-                    for (uint32_t j = 2; j < cnt; ++j) acc += Tl[s_ent[e + j]];
+                    for (uint32_t j = 2; j < cnt; ++j) acc += p[j * 33];
                 }
-                e += cnt;
+                p += cnt * 33;
                 if (!last) {
                     ys[l * 32 + lane] = acc;
                     return;
@@ -302,8 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 int32_t z;
                 if constexpr (E2) {
                     const float q = fmaf(acc, cs, s_coff[l]);
-                    qmax = fmaxf(qmax, fabsf(q));
-                    qnan = fmaf(q, 0.f, qnan);      // NaN / Inf detector
+                    qmax = fmax_nan_abs(qmax, q);
                     z = __float_as_int(__fadd_rd(q, 12582912.0f)) - 0x4B400000;  // floor(q), |q| < 2^22
                     f = (f ^ (uint64_t)(uint32_t)z) * LSHB_FNV_PRIME;
                 } else {
@@ -329,13 +350,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (!last) continue;
             if constexpr (E2) {
-                if (!(qmax < 4194304.0f) || qnan != 0.0f) {
-                    // rare: a code outside the fast floor range; redo this table exactly
+                if (!(qmax < 4194304.0f)) {
+                    // rare: a code outside the fast floor range (or NaN/Inf): redo this table exactly
                     f = LSHB_FNV_OFFSET;
+                    const float* p2 = T + (bpc[t * K] - cbase) * 33 + lane;
                     for (int kk = 0; kk < K; ++kk) {
                         const int l = t * K + kk;
                         float acc = first ? 0.0f : ys[l * 32 + lane];
-                        for (uint32_t j = bpc[l]; j < bpc[l + 1]; ++j) acc += Tl[s_ent[j]];
+                        const uint32_t cnt = bpc[l + 1] - bpc[l];
+                        for (uint32_t j = 0; j < cnt; ++j) acc += p2[j * 33];
+                        p2 += cnt * 33;
                         const int32_t z = floor_code(fmaf(acc, cs, s_coff[l]), dz.flags);
                         f = (f ^ (uint64_t)(uint32_t)z) * LSHB_FNV_PRIME;
                         if (KT == 0 && dbg && valid && out.codes) out.codes[row * m + l] = z;
