@@ -253,6 +253,9 @@ struct lsh_handle {
     int key_width = 64;
     SketchPlanDev plan{};
     DiscretizeDev disc{};
+    bool chunked = false;
+    ChunkedPlanDev cplan{};
+    void* d_cplan_mem = nullptr;
     uint16_t* d_entries = nullptr;
     uint32_t* d_binptr = nullptr;
     uint32_t* d_signs = nullptr;
@@ -274,6 +277,122 @@ struct lsh_index {
     cudaStream_t stream = nullptr;  // build stream: memory is freed stream-ordered on it
 };
 
+// Chunked plan (large d and/or m): tables in groups whose partial sums fit in
+// shared memory; per group, the coordinates whose bin lies in the group (ascending),
+// cut into chunks of <= 1024; per chunk, bin-sorted ranks.  See sketch_chunked.cu.
+static lsh_status build_chunked_plan(lsh_handle* H, const std::vector<int32_t>& bin, const std::vector<int8_t>& sgn) {
+    const lsh_params* p = &H->p;
+    const int d = (int)p->d, m = p->m, K = p->K, L = p->L;
+    const int Q = 1024;
+    const size_t budget = 232448;
+    int tables_per_group = 0;
+    for (int g = L; g >= 1; --g) {
+        if (chunked_smem_bytes(m, g * K) <= budget) {
+            tables_per_group = g;
+            break;
+        }
+    }
+    if (tables_per_group == 0) {
+        H->sketch_ok = false;
+        return LSH_OK;
+    }
+    // coordinates of each group in ascending order
+    const int ngroups = (L + tables_per_group - 1) / tables_per_group;
+    std::vector<std::vector<int32_t>> gcoords(ngroups);
+    for (int j = 0; j < d; ++j) gcoords[(bin[j] / K) / tables_per_group].push_back(j);
+    std::vector<ChunkInfoDev> chunks;
+    std::vector<int32_t> gcoord;
+    std::vector<uint16_t> pos;
+    std::vector<uint32_t> sgnb;
+    std::vector<uint32_t> bp;
+    std::vector<uint8_t> cnt;
+    int max_cnt = 0, gbins = 0;
+    bool vec_ok = true;
+    for (int g = 0; g < ngroups; ++g) {
+        const int t0 = g * tables_per_group, t1 = std::min(L, t0 + tables_per_group);
+        const int nb = (t1 - t0) * K, b0 = t0 * K;
+        gbins = std::max(gbins, nb);
+        const std::vector<int32_t>& cl = gcoords[g];
+        const int total = (int)cl.size();
+        const int nck = std::max(1, (total + Q - 1) / Q);
+        for (int c = 0; c < nck; ++c) {
+            const int k0 = c * Q, k1 = std::min(total, k0 + Q);
+            ChunkInfoDev ci{};
+            ci.Qc = k1 - k0;
+            ci.t0 = t0;
+            ci.t1 = t1;
+            ci.flags = (c == 0 ? 1 : 0) | (c == nck - 1 ? 2 : 0);
+            ci.coord_off = (uint32_t)gcoord.size();
+            ci.bp_off = (uint32_t)bp.size();
+            std::vector<uint32_t> cn(nb + 1, 0);
+            for (int k = k0; k < k1; ++k) cn[bin[cl[k]] - b0 + 1]++;
+            for (int b = 0; b < nb; ++b) {
+                max_cnt = std::max(max_cnt, (int)cn[b + 1]);
+                cnt.push_back((uint8_t)std::min<uint32_t>(cn[b + 1], 255));
+            }
+            cnt.push_back(0);
+            for (int b = 0; b < nb; ++b) cn[b + 1] += cn[b];
+            for (int b = 0; b <= nb; ++b) bp.push_back(cn[b]);
+            std::vector<uint32_t> cur(cn.begin(), cn.end() - 1);
+            for (int k = k0; k < k1; ++k) {
+                const int j = cl[k];
+                const size_t idx = gcoord.size();
+                gcoord.push_back(j);
+                pos.push_back((uint16_t)cur[bin[j] - b0]++);
+                if (sgnb.size() * 32 <= idx) sgnb.push_back(0);
+                if (sgn[j] < 0) sgnb[idx >> 5] |= 1u << (idx & 31);
+            }
+            // 128-bit staging needs every aligned group of 4 elements to be 4 contiguous
+            // inputs starting at a multiple of 4
+            if (ci.Qc % 4) vec_ok = false;
+            for (int k = 0; k + 3 < ci.Qc && vec_ok; k += 4) {
+                const int j = cl[k0 + k];
+                if (j % 4 || cl[k0 + k + 1] != j + 1 || cl[k0 + k + 2] != j + 2 || cl[k0 + k + 3] != j + 3)
+                    vec_ok = false;
+            }
+            chunks.push_back(ci);
+            // keep every chunk's element range 32-aligned in the sign bit array
+            while (gcoord.size() % 32) {
+                gcoord.push_back(0);
+                pos.push_back(0);
+            }
+            while (sgnb.size() * 32 < gcoord.size()) sgnb.push_back(0);
+        }
+    }
+    // one device allocation for the plan
+    const size_t b_ch = chunks.size() * sizeof(ChunkInfoDev), b_gc = gcoord.size() * 4, b_pos = pos.size() * 2,
+                 b_sg = sgnb.size() * 4, b_bp = bp.size() * 4, b_cn = cnt.size();
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    const size_t total = al(b_ch) + al(b_gc) + al(b_pos) + al(b_sg) + al(b_bp) + al(b_cn);
+    CK(cudaMalloc(&H->d_cplan_mem, total));
+    char* base = (char*)H->d_cplan_mem;
+    size_t o = 0;
+    auto put = [&](const void* src, size_t b) {
+        char* dst = base + o;
+        if (b) cudaMemcpy(dst, src, b, cudaMemcpyHostToDevice);
+        o += al(b);
+        return (void*)dst;
+    };
+    ChunkedPlanDev cp{};
+    cp.d = d;
+    cp.m = m;
+    cp.L = L;
+    cp.K = K;
+    cp.nchunks = (int)chunks.size();
+    cp.gbins = gbins;
+    cp.max_cnt = max_cnt;
+    cp.vec_ok = vec_ok ? 1 : 0;
+    cp.chunks = (const ChunkInfoDev*)put(chunks.data(), b_ch);
+    cp.gcoord = (const int32_t*)put(gcoord.data(), b_gc);
+    cp.pos = (const uint16_t*)put(pos.data(), b_pos);
+    cp.sgn = (const uint32_t*)put(sgnb.data(), b_sg);
+    cp.bp = (const uint32_t*)put(bp.data(), b_bp);
+    cp.cnt = (const uint8_t*)put(cnt.data(), b_cn);
+    H->cplan = cp;
+    H->chunked = true;
+    return LSH_OK;
+}
+
 static lsh_status build_plan(lsh_handle* H) {
     const lsh_params* p = &H->p;
     std::vector<int32_t> bin;
@@ -282,29 +401,20 @@ static lsh_status build_plan(lsh_handle* H) {
     const int d = (int)p->d, m = p->m;
     const int vpt = d <= 64 ? 1 : (d <= 256 ? 4 : 16);
     const int Q = 64 * vpt;
-    const int nchunks = (d + Q - 1) / Q;
-    if (sketch_smem_bytes(Q, m, d, nchunks) > 232448) {
-        H->sketch_ok = false;  // needs the structured HCS path (not in this build)
-        return LSH_OK;
-    }
+    if (d > Q || sketch_smem_bytes(Q, m, d, 1) > 232448) return build_chunked_plan(H, bin, sgn);
+    const int nchunks = 1;
     std::vector<uint32_t> bin_ptr((size_t)nchunks * (m + 1), 0);
     std::vector<uint16_t> pos(d);
     std::vector<uint32_t> sign_bits((d + 31) / 32, 0);
     for (int j = 0; j < d; ++j)
         if (sgn[j] < 0) sign_bits[j >> 5] |= 1u << (j & 31);
-    for (int c = 0; c < nchunks; ++c) {
-        const int j0 = c * Q, j1 = std::min(d, (c + 1) * Q);
-        uint32_t* bp = bin_ptr.data() + (size_t)c * (m + 1);
+    {
         std::vector<uint32_t> cnt(m + 1, 0);
-        for (int j = j0; j < j1; ++j) cnt[bin[j] + 1]++;
+        for (int j = 0; j < d; ++j) cnt[bin[j] + 1]++;
         for (int l = 0; l < m; ++l) cnt[l + 1] += cnt[l];
-        for (int l = 0; l <= m; ++l) bp[l] = (uint32_t)j0 + cnt[l];
+        for (int l = 0; l <= m; ++l) bin_ptr[l] = cnt[l];
         std::vector<uint32_t> cur(cnt.begin(), cnt.end() - 1);
-        for (int j = j0; j < j1; ++j) {  // ascending j inside each bin (deterministic summation order)
-            const int k = j - j0;
-            (void)k;
-            pos[j] = (uint16_t)(cur[bin[j]]++);
-        }
+        for (int j = 0; j < d; ++j) pos[j] = (uint16_t)(cur[bin[j]]++);  // ascending j inside each bin
     }
     CK(cudaMalloc(&H->d_entries, sizeof(uint16_t) * std::max(1, d)));
     CK(cudaMalloc(&H->d_binptr, sizeof(uint32_t) * bin_ptr.size()));
@@ -313,9 +423,7 @@ static lsh_status build_plan(lsh_handle* H) {
     CK(cudaMemcpy(H->d_binptr, bin_ptr.data(), sizeof(uint32_t) * bin_ptr.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(H->d_signs, sign_bits.data(), sizeof(uint32_t) * sign_bits.size(), cudaMemcpyHostToDevice));
     int max_cnt = 0;
-    for (int c = 0; c < nchunks; ++c)
-        for (int l = 0; l < m; ++l)
-            max_cnt = std::max(max_cnt, (int)(bin_ptr[(size_t)c * (m + 1) + l + 1] - bin_ptr[(size_t)c * (m + 1) + l]));
+    for (int l = 0; l < m; ++l) max_cnt = std::max(max_cnt, (int)(bin_ptr[l + 1] - bin_ptr[l]));
     H->plan = SketchPlanDev{d, m, p->L, p->K, Q, vpt, nchunks, max_cnt, H->d_entries, H->d_binptr, H->d_signs};
     return LSH_OK;
 }
@@ -324,6 +432,7 @@ static void free_handle(lsh_handle* H) {
     if (!H) return;
     cudaFree(H->d_entries);
     cudaFree(H->d_binptr);
+    cudaFree(H->d_cplan_mem);
     cudaFree(H->d_signs);
     cudaFree(H->d_coff);
     cudaFree(H->d_R);
@@ -444,7 +553,8 @@ static lsh_status hash_impl(const lsh_handle* H, const float* X, int64_t n, int6
     }
     if (!H->sketch_ok) return LSH_EUNSUPPORTED;
     timing_begin(tname, s);
-    cudaError_t e = launch_sketch(H->plan, H->disc, X, n, ld, out, H->num_sms, s);
+    cudaError_t e = H->chunked ? launch_sketch_chunked(H->cplan, H->disc, X, n, ld, out, H->num_sms, s)
+                               : launch_sketch(H->plan, H->disc, X, n, ld, out, H->num_sms, s);
     count_launch();
     timing_end(tname, s);
     if (e != cudaSuccess) return cuda_fail(e, "sketch");

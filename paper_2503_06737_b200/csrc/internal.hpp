@@ -29,6 +29,30 @@ struct SketchPlanDev {
     const uint32_t* sign_bits;  // [ceil(d/32)] bit j set = sign(j) = -1 (applied while staging)
 };
 
+// Chunked plan (sketch_chunked.cu): tables in groups, per group the coordinates
+// whose bin is in the group, in chunks of <= 1024.
+struct ChunkInfoDev {
+    int32_t Qc;         // coordinates in this chunk
+    int32_t t0, t1;     // tables of the chunk's group
+    int32_t flags;      // bit 0: first chunk of the group, bit 1: last chunk of the group
+    uint32_t coord_off; // offset of the chunk's first element in gcoord / pos / sgn
+    uint32_t bp_off;    // offset of the chunk's (t1-t0)*K+1 bin starts in bp / cnt
+    uint32_t pad0, pad1;
+};
+struct ChunkedPlanDev {
+    int d, m, L, K;
+    int nchunks;
+    int gbins;        // largest group size in bins (partial-sum buffer)
+    int max_cnt;      // largest coordinates-per-bin inside one chunk
+    int vec_ok;       // every aligned group of 4 chunk elements is 4 contiguous, 16B-aligned inputs
+    const ChunkInfoDev* chunks;
+    const int32_t* gcoord;   // global input coordinate of every chunk element
+    const uint16_t* pos;     // bin-sorted rank of every chunk element inside its chunk
+    const uint32_t* sgn;     // sign bit of every chunk element
+    const uint32_t* bp;      // bin start ranks (relative to the chunk)
+    const uint8_t* cnt;      // coordinates per bin in the chunk (saturated at 255)
+};
+
 struct DiscretizeDev {
     int e2lsh;                // 1: E2LSH floor codes + fingerprint keys; 0: SRP bits
     float c_scale;            // sqrt(m)/w (CS/HCS), 1/w (dense)
@@ -47,6 +71,9 @@ struct HashOut {
 cudaError_t launch_sketch(const SketchPlanDev& plan, const DiscretizeDev& disc, const float* X, int64_t n,
                           int64_t ld, HashOut out, int num_sms, cudaStream_t s);
 size_t sketch_smem_bytes(int Q, int m, int d, int nchunks);
+cudaError_t launch_sketch_chunked(const ChunkedPlanDev& plan, const DiscretizeDev& disc, const float* X, int64_t n,
+                                  int64_t ld, HashOut out, int num_sms, cudaStream_t s);
+size_t chunked_smem_bytes(int m, int gbins);
 
 cudaError_t launch_dense_gemm_f32(const float* X, int64_t n, int64_t ld, const uint16_t* Rbf16, int m, int d,
                                   float* Y, cudaStream_t s);

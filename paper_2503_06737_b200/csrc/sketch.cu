@@ -423,11 +423,9 @@ cudaError_t launch_sketch(const SketchPlanDev& plan, const DiscretizeDev& dz, co
             return vec ? launch_k<4, true, true>(plan, dz, X, n, ld, out, num_sms, s)
                        : launch_k<4, false, true>(plan, dz, X, n, ld, out, num_sms, s);
         case 16:
-            if (single)
-                return vec ? launch_k<16, true, true>(plan, dz, X, n, ld, out, num_sms, s)
-                           : launch_k<16, false, true>(plan, dz, X, n, ld, out, num_sms, s);
-            return vec ? launch_k<16, true, false>(plan, dz, X, n, ld, out, num_sms, s)
-                       : launch_k<16, false, false>(plan, dz, X, n, ld, out, num_sms, s);
+            if (!single) return cudaErrorInvalidValue;  // multi-chunk plans run sketch_chunked.cu
+            return vec ? launch_k<16, true, true>(plan, dz, X, n, ld, out, num_sms, s)
+                       : launch_k<16, false, true>(plan, dz, X, n, ld, out, num_sms, s);
         default:
             return cudaErrorInvalidValue;
     }

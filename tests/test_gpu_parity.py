@@ -232,3 +232,33 @@ def test_empty_index():
     idx = h.build_index(torch.zeros((0, 64), device="cuda"))
     ids, uk, of = idx.view(0)
     assert ids.numel() == 0 and uk.numel() == 0 and of.cpu().tolist() == [0]
+
+
+@pytest.mark.parametrize("scheme", ["HCS_E2LSH", "HCS_SRP"])
+def test_c5_full_size_sampled(scheme):
+    """C5 (d = 65536 = 16^4, m = 4096 = 8^4): chunked/grouped plan at full n, sampled rows."""
+    c = synth.CONFIGS["C5"]
+    p = _params(c, scheme)
+    h = _handle(p)
+    X = synth.rows(c, 0, c.n, device="cuda")
+    keys = h.hash(X, keys=True)["keys"]
+    torch.cuda.synchronize()
+    h.check()
+    g = np.random.default_rng(5)
+    rows = np.concatenate([np.arange(96), np.sort(g.choice(np.arange(96, c.n), 96, replace=False))])
+    ridx = torch.from_numpy(rows).cuda()
+    Xs = X[ridx].contiguous()
+    del X
+    # full debug comparison on the sampled rows (same kernels, smaller launch)
+    _h, out, ref = _compare(p, Xs, Xs.cpu().numpy(), h=h)
+    kr = parity.check_keys(p, ref, keys.view(torch.int64)[:, ridx].cpu().numpy().view(np.uint64))
+    assert kr["mismatch_outside_exempt"] == 0, kr
+
+
+@pytest.mark.parametrize("scheme,d,m,L,K", [("CS_E2LSH", 2100, 2048, 128, 16), ("CS_SRP", 3000, 4096, 256, 16),
+                                            ("HCS_SRP", 6000, 1024, 64, 16)])
+def test_grouped_chunked_plans(scheme, d, m, L, K):
+    kw = dict(mode_d=(10, 25, 25), mode_m=(8, 8, 16)) if scheme.startswith("HCS") else {}
+    p = lsh.Params(scheme, d=d, m=m, L=L, K=K, w=3.0, seed=11, **kw)
+    X = synth.gaussian_rows_like(333, d, 21, device="cuda")
+    _compare(p, X, X.cpu().numpy())
