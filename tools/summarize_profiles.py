@@ -53,7 +53,7 @@ if os.path.exists(rep):
             for w, v in vals.items():
                 f.write(f"   {w:60s} {v} {rows[1][idx[w]]}\n")
     for name, vals in lines:
-        if name.startswith("lshb::sketch_kernel"):
+        if "sketch_kernel" in name:
             try:
                 mult = lambda u: {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9}.get(u.strip().lower(), 1)
                 rd = float(vals["dram__bytes_read.sum"].replace(",", "")) * mult(rows[1][idx["dram__bytes_read.sum"]])
