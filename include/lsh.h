@@ -157,6 +157,15 @@ lsh_status lsh_query_buckets(const lsh_handle* h, const lsh_index* idx, const fl
  * 1 <= B <= 20. */
 lsh_status lsh_index_counts(const lsh_index* idx, int32_t B, uint32_t* counts, void* stream);
 
+/* Multi-GPU exchange step (§8(e)): given the all-gathered coarse counts of every rank,
+ * all_counts uint32 [G][L][2^B] (device), write offsets int64 [L][2^B] (device): the
+ * global position where rank `rank`'s run of (table t, coarse bin b) starts in the
+ * global bin-major / rank-minor order,
+ *   offsets[t][b] = sum_{b'<b} sum_r all_counts[r][t][b'] + sum_{r'<rank} all_counts[r'][t][b].
+ * 0 <= rank < G, 1 <= B <= 20.  Asynchronous. */
+lsh_status lsh_global_offsets(const uint32_t* all_counts, int32_t G, int32_t rank, int32_t L, int32_t B,
+                              int64_t* offsets, void* stream);
+
 /* ---- parameters, errors, instrumentation -------------------------------- */
 
 typedef enum {

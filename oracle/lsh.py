@@ -387,3 +387,18 @@ def projection_op_count(p: Params, t: Tables, x: np.ndarray) -> int:
     else:
         cs_sketch(x, t.h[0], t.s[0], p.m, ops)
     return ops[0]
+
+
+def global_coarse_offsets(all_counts: np.ndarray, rank: int) -> np.ndarray:
+    """Global start of rank `rank`'s run of every (table, coarse bin).
+
+    offset[t][b] = sum_{b' < b} sum_r counts[r][t][b']  +  sum_{r' < rank} counts[r'][t][b]
+    i.e. the concatenation order is bin-major, rank-minor, matching the G=1 order
+    of buckets (coarse bins ascend with the key) with ids ascending across ranks.
+    """
+    c = np.asarray(all_counts, dtype=np.int64)          # [G][L][2^B]
+    totals = c.sum(axis=0)                              # [L][2^B]
+    before_bins = np.concatenate([np.zeros((totals.shape[0], 1), np.int64),
+                                  np.cumsum(totals, axis=1)[:, :-1]], axis=1)
+    before_ranks = c[:rank].sum(axis=0) if rank > 0 else np.zeros_like(totals)
+    return before_bins + before_ranks

@@ -61,6 +61,7 @@ def lib() -> ctypes.CDLL:
         "lsh_index_destroy": (None, [vp]),
         "lsh_query_buckets": (i32, [vp, vp, vp, i64, i64, vp, vp, vp]),
         "lsh_index_counts": (i32, [vp, i32, vp, vp]),
+        "lsh_global_offsets": (i32, [vp, i32, i32, i32, i32, vp, vp]),
         "lsh_export_host": (i32, [P(lsh_params), i32, i32, vp, P(sz)]),
         "lsh_get_params": (i32, [vp, i32, i32, vp, P(sz)]),
         "lsh_check": (i32, [vp]),
@@ -136,6 +137,19 @@ def timing_get(name: str) -> Tuple[float, int]:
     ms, n = ctypes.c_double(0), ctypes.c_int64(0)
     _check(lib().lsh_timing_get(name.encode(), ctypes.byref(ms), ctypes.byref(n)), "lsh_timing_get")
     return ms.value, n.value
+
+
+def global_offsets(all_counts, rank: int, stream=None):
+    """lsh_global_offsets: all_counts int32/uint32 [G, L, 2^B] (CUDA) -> int64 [L, 2^B]."""
+    torch = _torch()
+    G, L, nb = all_counts.shape
+    B = nb.bit_length() - 1
+    if (1 << B) != nb:
+        raise ValueError("last dimension must be 2^B")
+    out = torch.empty((L, nb), dtype=torch.int64, device=all_counts.device)
+    _check(lib().lsh_global_offsets(_dev_ptr(all_counts.contiguous(), name="all_counts"), G, rank, L, B,
+                                    out.data_ptr(), _stream_ptr(stream)), "lsh_global_offsets")
+    return out
 
 
 def _torch():

@@ -743,6 +743,18 @@ extern "C" lsh_status lsh_index_counts(const lsh_index* idx, int32_t B, uint32_t
     return LSH_OK;
 }
 
+extern "C" lsh_status lsh_global_offsets(const uint32_t* all_counts, int32_t G, int32_t rank, int32_t L, int32_t B,
+                                        int64_t* offsets, void* stream) {
+    if (G < 1 || rank < 0 || rank >= G || L < 1 || B < 1 || B > 20 || !all_counts || !offsets) return LSH_EDIM;
+    cudaStream_t s = (cudaStream_t)stream;
+    timing_begin("global_offsets", s);
+    cudaError_t e = launch_global_offsets(all_counts, G, rank, L, B, offsets, s);
+    count_launch();
+    timing_end("global_offsets", s);
+    if (e != cudaSuccess) return cuda_fail(e, "global_offsets");
+    return LSH_OK;
+}
+
 // ---------------------------------------------------------------------------
 // parameter export
 // ---------------------------------------------------------------------------

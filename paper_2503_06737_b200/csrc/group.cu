@@ -562,6 +562,58 @@ __global__ void counts_kernel(IndexDev idx, int64_t n, int L, int W, int B, uint
     atomicAdd(&counts[((int64_t)t << B) + bin], sz);
 }
 
+// Exclusive prefix of the all-gathered coarse counts (bin-major, rank-minor), one
+// block per table: scan over bins of the totals, plus the counts of lower ranks.
+__global__ void __launch_bounds__(1024) global_offsets_kernel(const uint32_t* __restrict__ all, int G, int rank, int L,
+                                                             int B, int64_t* __restrict__ off) {
+    __shared__ unsigned long long wsum[32];
+    __shared__ unsigned long long carry_s;
+    const int t = blockIdx.x;
+    const int nb = 1 << B;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) carry_s = 0;
+    __syncthreads();
+    for (int base = 0; base < nb; base += 1024) {
+        const int b = base + threadIdx.x;
+        unsigned long long tot = 0, lower = 0;
+        if (b < nb) {
+            for (int r = 0; r < G; ++r) {
+                const unsigned long long c = all[((int64_t)r * L + t) * nb + b];
+                tot += c;
+                if (r < rank) lower += c;
+            }
+        }
+        unsigned long long x = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            unsigned long long w = wsum[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += y;
+            }
+            wsum[lane] = w;
+        }
+        __syncthreads();
+        const unsigned long long excl = carry_s + (warp ? wsum[warp - 1] : 0ull) + x - tot;
+        if (b < nb) off[(int64_t)t * nb + b] = (int64_t)(excl + lower);
+        __syncthreads();
+        if (threadIdx.x == 1023) carry_s = excl + tot;
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_global_offsets(const uint32_t* all, int G, int rank, int L, int B, int64_t* off, cudaStream_t s) {
+    global_offsets_kernel<<<L, 1024, 0, s>>>(all, G, rank, L, B, off);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_counts(const IndexDev& idx, int64_t n, int L, int W, int B, uint32_t* counts, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(uint32_t) * ((size_t)L << B), s);
     if (e != cudaSuccess || n == 0) return e;

@@ -102,6 +102,7 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
                          GroupScratch& sc, IndexDev& out, int* flags, cudaStream_t s);
 cudaError_t launch_lookup(const uint64_t* qkeys, int64_t nq, int L, int64_t n, const IndexDev& idx,
                           int64_t* begin, int64_t* end, cudaStream_t s);
+cudaError_t launch_global_offsets(const uint32_t* all, int G, int rank, int L, int B, int64_t* off, cudaStream_t s);
 cudaError_t launch_counts(const IndexDev& idx, int64_t n, int L, int width, int B, uint32_t* counts,
                           cudaStream_t s);
 

@@ -262,3 +262,26 @@ def test_grouped_chunked_plans(scheme, d, m, L, K):
     p = lsh.Params(scheme, d=d, m=m, L=L, K=K, w=3.0, seed=11, **kw)
     X = synth.gaussian_rows_like(333, d, 21, device="cuda")
     _compare(p, X, X.cpu().numpy())
+
+
+@pytest.mark.parametrize("G,L,B", [(1, 3, 4), (4, 7, 12), (8, 64, 12), (3, 2, 20)])
+def test_global_offsets_kernel(G, L, B):
+    import paper_2503_06737_b200 as pk
+    g = np.random.default_rng(G * 100 + B)
+    allc = g.integers(0, 1000, (G, L, 1 << B)).astype(np.int32)
+    dev = torch.from_numpy(allc).cuda()
+    for r in range(G):
+        got = pk.global_offsets(dev, r).cpu().numpy()
+        assert np.array_equal(got, lsh.global_coarse_offsets(allc, r)), r
+
+
+def test_build_index_sharded_single_rank():
+    from paper_2503_06737_b200.dist import build_index_sharded
+    c = synth.CONFIGS["C2"]
+    p = _params(c, "CS_SRP")
+    h = _handle(p)
+    X = synth.rows(c, 0, 5000, device="cuda")
+    sh = build_index_sharded(h, X, id_base=0, B=8)
+    keys = h.hash(X, keys=True)["keys"].cpu().numpy()
+    assert np.array_equal(sh.counts.cpu().numpy().astype(np.uint32), lsh.coarse_counts(p, keys, 8))
+    assert np.array_equal(sh.offsets.cpu().numpy(), lsh.global_coarse_offsets(sh.all_counts.cpu().numpy(), 0))
