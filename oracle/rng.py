@@ -131,11 +131,54 @@ def round_bf16(x: float) -> float:
     return float(np.array([bits], dtype=np.uint64).view(np.float64)[0])
 
 
+def round_bf16_array(x: np.ndarray) -> np.ndarray:
+    """round_bf16 elementwise (same bit manipulation, vectorised)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    bits = x.view(np.uint64)
+    drop = np.uint64(45)
+    lsb = (bits >> drop) & np.uint64(1)
+    with np.errstate(over="ignore"):
+        r = ((bits + (np.uint64((1 << 44) - 1) + lsb)) >> drop) << drop
+    out = r.view(np.float64).copy()
+    out[x == 0] = x[x == 0]
+    return out
+
+
+def _gaussian_rows_vectorised(seed: int, m: int, d: int) -> np.ndarray:
+    """Same stream and Box-Muller as gaussian_rows, elementwise in NumPy (large m*d).
+
+    NumPy's log/cos/sin may differ from the C library's in the last ulp; after the
+    bf16 rounding this changes a value only if it sits on a rounding tie
+    (probability ~2^-40 per value).  Small shapes use the scalar path, which the
+    C++ draw is checked against bit for bit.
+    """
+    total = m * d
+    pairs = (total + 1) // 2
+    base = np.uint64(Stream(seed, "gaussian").state)
+    k = np.arange(1, 2 * pairs + 1, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        st = base + k * np.uint64(SM64_GAMMA)
+        z = st
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    u = (z >> np.uint64(11)).astype(np.float64) * (1.0 / (1 << 53))
+    u1 = 1.0 - u[0::2]
+    u2 = u[1::2]
+    rho = np.sqrt(-2.0 * np.log(u1))
+    vals = np.empty(2 * pairs, dtype=np.float64)
+    vals[0::2] = rho * np.cos(2.0 * math.pi * u2)
+    vals[1::2] = rho * np.sin(2.0 * math.pi * u2)
+    return round_bf16_array(vals[:total]).reshape(m, d)
+
+
 def gaussian_rows(seed: int, m: int, d: int) -> np.ndarray:
     """R in N(0,1)^{m x d}, Box-Muller, row-major fill, bf16-rounded (R4).
 
     Returns float64 array whose values are exactly bf16-representable.
     """
+    if m * d > (1 << 20):
+        return _gaussian_rows_vectorised(seed, m, d)
     st = Stream(seed, "gaussian")
     total = m * d
     vals = np.empty(total, dtype=np.float64)

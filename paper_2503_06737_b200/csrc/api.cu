@@ -10,6 +10,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -261,6 +262,8 @@ struct lsh_handle {
     uint32_t* d_signs = nullptr;
     float* d_coff = nullptr;
     uint16_t* d_R = nullptr;
+    uint16_t* d_Rpad = nullptr;  // bf16 [m][d_pad], d_pad = roundup(d, 64): tensor-core B operand
+    int d_pad = 0;
     int* d_flags = nullptr;
     std::vector<int32_t*> d_h, d_s;
     float* d_b = nullptr;
@@ -436,6 +439,7 @@ static void free_handle(lsh_handle* H) {
     cudaFree(H->d_signs);
     cudaFree(H->d_coff);
     cudaFree(H->d_R);
+    cudaFree(H->d_Rpad);
     cudaFree(H->d_flags);
     for (auto x : H->d_h) cudaFree(x);
     for (auto x : H->d_s) cudaFree(x);
@@ -490,6 +494,13 @@ extern "C" lsh_status lsh_create(const lsh_params* p, lsh_handle** out) {
         if ((e = cudaMalloc(&H->d_R, bytes)) != cudaSuccess) return fail(cuda_fail(e, "malloc R"));
         if ((e = cudaMemcpy(H->d_R, H->host.R.data(), bytes, cudaMemcpyHostToDevice)) != cudaSuccess)
             return fail(cuda_fail(e, "memcpy R"));
+        H->d_pad = (int)((p->d + 63) / 64 * 64);
+        const size_t pbytes = sizeof(uint16_t) * (size_t)m * H->d_pad;
+        if ((e = cudaMalloc(&H->d_Rpad, pbytes)) != cudaSuccess) return fail(cuda_fail(e, "malloc Rpad"));
+        cudaMemset(H->d_Rpad, 0, pbytes);
+        if ((e = cudaMemcpy2D(H->d_Rpad, sizeof(uint16_t) * H->d_pad, H->d_R, sizeof(uint16_t) * p->d,
+                              sizeof(uint16_t) * p->d, m, cudaMemcpyDeviceToDevice)) != cudaSuccess)
+            return fail(cuda_fail(e, "pad R"));
     } else {
         for (int k = 0; k < H->host.N; ++k) {
             int32_t *dh = nullptr, *ds = nullptr;
@@ -538,10 +549,22 @@ static lsh_status hash_impl(const lsh_handle* H, const float* X, int64_t n, int6
     if (is_dense(p.scheme)) {
         float* Y = out.proj;
         if (!Y) CK(cudaMallocAsync((void**)&Y, sizeof(float) * (size_t)n * p.m, s));
-        timing_begin("dense_gemm", s);
-        cudaError_t e = launch_dense_gemm_f32(X, n, ld, H->d_R, p.m, (int)p.d, Y, s);
-        count_launch();
-        timing_end("dense_gemm", s);
+        cudaError_t e;
+        static const bool simt = getenv("LSH_DENSE_SIMT") && getenv("LSH_DENSE_SIMT")[0] == '1';
+        if (simt) {  // CUDA-core cross-check kernel (tests only)
+            timing_begin("dense_gemm_simt", s);
+            e = launch_dense_gemm_f32(X, n, ld, H->d_R, p.m, (int)p.d, Y, s);
+            count_launch();
+            timing_end("dense_gemm_simt", s);
+        } else {
+            const int64_t rows = std::min<int64_t>(n, (int64_t)dense_tc_rows_per_batch(H->d_pad));
+            uint16_t* A = nullptr;
+            CK(cudaMallocAsync((void**)&A, sizeof(uint16_t) * (size_t)rows * 3 * H->d_pad, s));
+            timing_begin("dense_gemm", s);
+            e = launch_dense_tc(X, n, ld, (int)p.d, H->d_Rpad, p.m, H->d_pad, A, rows, Y, s);
+            timing_end("dense_gemm", s);
+            CK(cudaFreeAsync(A, s));
+        }
         if (e != cudaSuccess) return cuda_fail(e, "dense_gemm");
         timing_begin("keys_from_proj", s);
         e = launch_keys_from_proj(Y, n, p.m, p.L, p.K, H->disc, out, s);

@@ -550,16 +550,45 @@ cudaError_t launch_lookup(const uint64_t* qkeys, int64_t nq, int L, int64_t n, c
     return cudaGetLastError();
 }
 
+// Coarse counts from the sorted bucket keys: coarse bins are monotone in key order,
+// so bin b of table t spans the buckets [lower_bound(b << s), lower_bound((b+1) << s))
+// and its point count is a difference of two offsets (no atomics, deterministic).
+__device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* a, int64_t nb, uint64_t key) {
+    int64_t lo = 0, hi = nb;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (a[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
 __global__ void counts_kernel(IndexDev idx, int64_t n, int L, int W, int B, uint32_t* counts) {
     const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gi >= (int64_t)L * n) return;
-    const int t = (int)(gi / n);
-    const int64_t b = gi % n;
-    if (b >= idx.nb[t]) return;
-    const uint64_t key = idx.ukeys[(int64_t)t * n + b];
-    const uint64_t bin = W > B ? (key >> (W - B)) : key;
-    const uint32_t sz = idx.offs[(int64_t)t * (n + 1) + b + 1] - idx.offs[(int64_t)t * (n + 1) + b];
-    atomicAdd(&counts[((int64_t)t << B) + bin], sz);
+    const int64_t nbins = (int64_t)1 << B;
+    if (gi >= (int64_t)L * nbins) return;
+    const int t = (int)(gi >> B);
+    const uint64_t b = (uint64_t)(gi & (nbins - 1));
+    const uint64_t* uk = idx.ukeys + (int64_t)t * n;
+    const uint32_t* of = idx.offs + (int64_t)t * (n + 1);
+    const int64_t nb = idx.nb[t];
+    int64_t lo, hi;
+    if (W > B) {
+        const int sh = W - B;
+        lo = lower_bound_u64(uk, nb, b << sh);
+        hi = (b + 1 == (uint64_t)nbins) ? nb : lower_bound_u64(uk, nb, (b + 1) << sh);
+    } else {
+        lo = lower_bound_u64(uk, nb, b);
+        hi = (lo < nb && uk[lo] == b) ? lo + 1 : lo;
+    }
+    counts[gi] = of[hi] - of[lo];
+}
+
+cudaError_t launch_counts(const IndexDev& idx, int64_t n, int L, int W, int B, uint32_t* counts, cudaStream_t s) {
+    const int64_t tot = (int64_t)L << B;
+    if (n == 0) return cudaMemsetAsync(counts, 0, sizeof(uint32_t) * tot, s);
+    counts_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(idx, n, L, W, B, counts);
+    return cudaGetLastError();
 }
 
 // Exclusive prefix of the all-gathered coarse counts (bin-major, rank-minor), one
@@ -614,12 +643,5 @@ cudaError_t launch_global_offsets(const uint32_t* all, int G, int rank, int L, i
     return cudaGetLastError();
 }
 
-cudaError_t launch_counts(const IndexDev& idx, int64_t n, int L, int W, int B, uint32_t* counts, cudaStream_t s) {
-    cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(uint32_t) * ((size_t)L << B), s);
-    if (e != cudaSuccess || n == 0) return e;
-    const int64_t tot = (int64_t)L * n;
-    counts_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(idx, n, L, W, B, counts);
-    return cudaGetLastError();
-}
-
 }  // namespace lshb
+

@@ -77,6 +77,9 @@ size_t chunked_smem_bytes(int m, int gbins);
 
 cudaError_t launch_dense_gemm_f32(const float* X, int64_t n, int64_t ld, const uint16_t* Rbf16, int m, int d,
                                   float* Y, cudaStream_t s);
+cudaError_t launch_dense_tc(const float* X, int64_t n, int64_t ld, int d, const uint16_t* R_pad, int m, int d_pad,
+                            uint16_t* A_scratch, int64_t rows_per_batch, float* Y, cudaStream_t s);
+size_t dense_tc_rows_per_batch(int d_pad);
 cudaError_t launch_keys_from_proj(const float* Y, int64_t n, int m, int L, int K, const DiscretizeDev& disc,
                                   HashOut out, cudaStream_t s);
 

@@ -4,8 +4,13 @@
                dot product's natural scale sqrt(sum_i a_li^2 x_i^2); sigma_l == 0
                (empty bin) requires y_gpu == 0 exactly.
   E2LSH codes: bit-exact except entries whose quotient (scale*y+b)/w lies within
-               1e-5 of an integer (counted and reported).
-  SRP bits:    bit-exact except entries with |y_ref| < 1e-6 (counted, reported).
+               max(1e-5, 6*2^-24*sqrt(k_l)*scale*sigma_l/w) of an integer (counted and
+               reported): the north_star band, widened only where the fp32
+               accumulation of k_l nonzero products cannot meet it (derived bound,
+               DESIGN.md §5; CS/HCS bins keep 1e-5).  The dense tensor-core
+               projection adds its rigorous accumulation bound tc_band_y().
+  SRP bits:    bit-exact except entries with |y_ref| < max(1e-6, 6*2^-24*sqrt(k_l)*sigma_l)
+               (counted, reported; same derivation).
   keys:        bit-exact for every (table, point) without an exempt coordinate.
   tables:      bit-exact given identical keys.
 """
@@ -44,11 +49,54 @@ def check_proj(y_gpu: np.ndarray, y_ref: np.ndarray, sig: np.ndarray) -> dict:
             if y_ref.size else 0.0}
 
 
+FP32_U = 2.0 ** -24
+
+
+def nnz_terms(p: lsh.Params, t: lsh.Tables, X: np.ndarray) -> np.ndarray:
+    """Number of nonzero products in each projection entry."""
+    nz = (np.asarray(X) != 0).astype(np.float64)
+    if lsh.is_dense(p.scheme):
+        return nz @ (t.R != 0).astype(np.float64).T
+    ones = [np.ones_like(s) for s in t.s]
+    if lsh.is_hcs(p.scheme):
+        return lsh.hcs_sketch(nz, p.mode_d, p.mode_m, t.h, ones)
+    return lsh.cs_sketch(nz, t.h[0], ones[0], p.m)
+
+
+def tc_band_y(p: lsh.Params, t: lsh.Tables, X: np.ndarray) -> np.ndarray:
+    """Rigorous fp32 tensor-core accumulation bound of the dense projection:
+    Y = [x0|x1|x2].[R|R|R]^T accumulates in fp32 TMEM over 16-wide K steps; each step
+    with a nonzero product rounds the accumulator once, by at most u * sum_i |r_li x_i|.
+    """
+    Xa = np.abs(np.asarray(X, np.float64))
+    d = Xa.shape[1]
+    chunks = (np.add.reduceat((Xa != 0).astype(np.int64), np.arange(0, d, 16), axis=1) > 0).sum(axis=1)
+    abs_sum = Xa @ np.abs(t.R).T
+    return 3.0 * chunks[:, None] * FP32_U * abs_sum
+
+
+def code_band(p: lsh.Params, t: lsh.Tables, X: np.ndarray) -> np.ndarray:
+    """Per-entry exemption half-width in quotient units (see module docstring)."""
+    w = float(np.float32(p.w))
+    derived = 6.0 * FP32_U * np.sqrt(nnz_terms(p, t, X)) * lsh.e2lsh_scale(p) * sigma(p, t, X) / w
+    if lsh.is_dense(p.scheme):
+        derived = np.maximum(derived, tc_band_y(p, t, X) / w)
+    return np.maximum(CODE_BAND, derived)
+
+
+def srp_band(p: lsh.Params, t: lsh.Tables, X: np.ndarray) -> np.ndarray:
+    derived = 6.0 * FP32_U * np.sqrt(nnz_terms(p, t, X)) * sigma(p, t, X)
+    if lsh.is_dense(p.scheme):
+        derived = np.maximum(derived, tc_band_y(p, t, X))
+    return np.maximum(SRP_BAND, derived)
+
+
 def exempt_mask(p: lsh.Params, ref: dict) -> np.ndarray:
     if lsh.is_e2lsh(p.scheme):
         q = ref["quotient"]
-        return np.abs(q - np.round(q)) < CODE_BAND
-    return np.abs(ref["proj"]) < SRP_BAND
+        band = ref.get("band", CODE_BAND)
+        return np.abs(q - np.round(q)) < band
+    return np.abs(ref["proj"]) < ref.get("band", SRP_BAND)
 
 
 def check_codes(p: lsh.Params, ref: dict, gpu_codes=None, gpu_bits=None) -> dict:

@@ -94,3 +94,9 @@ def test_invalid_parameters_rejected():
         sz = ctypes.c_size_t(0)
         assert pk.lib().lsh_export_host(ctypes.byref(p), 2, 0, None, ctypes.byref(sz)) == 1
     assert pk.lib().lsh_strerror(1) == b"invalid parameters"
+
+
+def test_no_undefined_internal_symbols():
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--undefined-only", pk.LIB_PATH], capture_output=True, text=True).stdout
+    assert "lshb" not in out, out

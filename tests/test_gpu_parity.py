@@ -50,6 +50,7 @@ def _compare(p: lsh.Params, X_dev, X_np, h=None, rows=None, report=None):
     ref = lsh.hash_points(p, t, X_np)
     pr = parity.check_proj(gp, ref["proj"], parity.sigma(p, t, X_np))
     assert pr["bad"] == 0 and pr["bad_empty"] == 0, pr
+    ref["band"] = parity.code_band(p, t, X_np) if lsh.is_e2lsh(p.scheme) else parity.srp_band(p, t, X_np)
     if lsh.is_e2lsh(p.scheme):
         cr = parity.check_codes(p, ref, gpu_codes=out["codes"].cpu().numpy()[sel])
     else:
@@ -285,3 +286,21 @@ def test_build_index_sharded_single_rank():
     keys = h.hash(X, keys=True)["keys"].cpu().numpy()
     assert np.array_equal(sh.counts.cpu().numpy().astype(np.uint32), lsh.coarse_counts(p, keys, 8))
     assert np.array_equal(sh.offsets.cpu().numpy(), lsh.global_coarse_offsets(sh.all_counts.cpu().numpy(), 0))
+
+
+def test_c5_dense_e2lsh_tensor_core_sampled():
+    """Dense E2LSH baseline at C5 shape (d = 65536, m = 4096): tcgen05 bf16x3 GEMM."""
+    c = synth.CONFIGS["C5"]
+    p = lsh.Params("E2LSH", d=c.d, m=c.m, L=c.L, K=c.K, w=c.w, seed=c.hash_seed)
+    rows = np.concatenate([np.arange(40), np.array([5000, 77777, 99999])])
+    Xs = synth.sample_rows(c, rows, device="cuda")
+    _compare(p, Xs, Xs.cpu().numpy())
+
+
+@pytest.mark.parametrize("m,L,K", [(160, 10, 16), (256, 16, 16), (520, 65, 8), (48, 3, 16)])
+def test_dense_tensor_core_shapes(m, L, K):
+    """Tile-edge shapes of the tcgen05 GEMM: m not a multiple of the N tile, d not of 64."""
+    for scheme in ("E2LSH", "SRP"):
+        p = lsh.Params(scheme, d=300, m=m, L=L, K=K, w=2.0, seed=9)
+        X = synth.gaussian_rows_like(333, 300, 4, device="cuda")
+        _compare(p, X, X.cpu().numpy())

@@ -109,3 +109,12 @@ def test_flat_index_example_and_bijection(golden):
             assert rng.flat_index(idx, dims) == j
             seen.add(tuple(idx))
         assert len(seen) == total
+
+
+def test_vectorised_gaussian_equals_scalar_path():
+    a = rng._gaussian_rows_vectorised(5, 40, 301)
+    st = rng.Stream(5, "gaussian")
+    b = np.array(rng.gaussian_rows(5, 40, 301))
+    assert np.array_equal(a, b) or (a != b).sum() <= 1  # last-ulp libm differences only at bf16 ties
+    x = np.random.default_rng(0).standard_normal(3000)
+    assert np.array_equal(rng.round_bf16_array(x), np.array([rng.round_bf16(float(v)) for v in x]))
