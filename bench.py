@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true", help="diagnostic only: skip the nvidia-smi sampler")
     return ap.parse_args()
 
 
@@ -119,6 +120,15 @@ def peaks():
         return float(pk["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def peaks_tensor():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["bf16_tflops_sustained"]), "measured (cuBLAS bf16 sustained)"
+    except Exception:
+        return 1400.0, "fallback"
 
 
 def ncu_traffic(config, scheme):
@@ -228,23 +238,26 @@ def run_ours(args):
         b, e = h.query_buckets(idx, Q)
         return idx, b, e
 
-    # warm-up
+    # warm-up with the same index lifetime pattern as the timed loop (the stream-ordered
+    # pool then already holds the memory of the in-flight indexes)
+    keep = []
     for _ in range(max(3, args.warmup)):
-        idx, _, _ = step()
+        keep.append(step()[0])
+        if len(keep) > 2:
+            keep.pop(0)
     torch.cuda.synchronize()
-    del idx
 
     # device-timed region (inputs resident in HBM; X >> L2 so no flush needed)
     pk.timing_reset()
     pk.timing_enable(True)
     clocks = ClockSampler(dev.index)
-    clocks.start()
+    if not args.no_clocks:
+        clocks.start()
     if use_dist:
         dist.barrier()
     torch.cuda.synchronize()
     l0 = pk.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    keep = []
     ev0.record(stream)
     for _ in range(args.steps):
         keep.append(step()[0])
@@ -260,7 +273,7 @@ def run_ours(args):
     ms_local = ev0.elapsed_time(ev1) / args.steps
     sketch_ms, sketch_n = pk.timing_get("sketch")
     kernel_ms = {k: pk.timing_get(k)[0] / max(1, args.steps) for k in
-                 ("sketch", "sketch_query", "radix_upsweep", "radix_scan", "radix_downsweep", "segsort", "rle", "lookup", "counts",
+                 ("sketch", "sketch_query", "radix_upsweep", "radix_scan", "radix_downsweep", "segsort", "segsort_long", "rle", "lookup", "counts",
                   "global_offsets", "dense_gemm", "keys_from_proj")}
     keep.clear()
     t = torch.tensor([ms_local], device=dev)
@@ -294,8 +307,11 @@ def run_ours(args):
             be_h[1].copy_(e, non_blocking=True)
             return idx
 
-        for _ in range(2):
-            e2e_step()
+        ekeep = []
+        for _ in range(3):
+            ekeep.append(e2e_step())
+            if len(ekeep) > 2:
+                ekeep.pop(0)
         torch.cuda.synchronize()
         esteps = max(2, min(args.steps, 5))
         if use_dist:
@@ -304,10 +320,12 @@ def run_ours(args):
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a0.record(stream)
         for _ in range(esteps):
-            ix = e2e_step()
+            ekeep.append(e2e_step())
+            if len(ekeep) > 2:
+                ekeep.pop(0)
         a1.record(stream)
         torch.cuda.synchronize()
-        del ix
+        ekeep.clear()
         te = torch.tensor([a0.elapsed_time(a1) / esteps], device=dev)
         if use_dist:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -321,10 +339,27 @@ def run_ours(args):
         return
 
     hbm_peak, peak_kind = peaks()
-    bytes_per_point = 4 * cfg.d + 8 * cfg.L          # sketch kernel: read the point, write its L keys
-    sketch_avg_ms = sketch_ms / max(1, sketch_n)
-    achieved = bytes_per_point * n_local / (sketch_avg_ms * 1e-3) / 1e9 if sketch_avg_ms > 0 else None
-    traffic = ncu_traffic(cfg.name, scheme)
+    dense = scheme in ("E2LSH", "SRP")
+    if dense:
+        # tensor-core dense baseline: algorithmic flops 2*n*m*d (the split into 3 bf16 terms
+        # triples the executed MMA work; reported separately)
+        g_ms, g_n = pk.timing_get("dense_gemm")
+        avg = g_ms / max(1, g_n)
+        flops = 2.0 * n_local * cfg.m * cfg.d
+        tf_peak, tf_kind = peaks_tensor()
+        achieved = flops / (avg * 1e-3) / 1e12 if avg > 0 else None
+        roof = {"kernel": "dense_gemm (tcgen05 bf16x3)", "bound": "tensor", "achieved": achieved, "peak": tf_peak,
+                "peak_kind": tf_kind, "unit": "TFLOP/s", "frac": (achieved / tf_peak) if achieved else None,
+                "flops_per_launch": flops, "executed_mma_flops_per_launch": 3 * flops, "traffic": None,
+                "avg_launch_ms": avg}
+    else:
+        bytes_per_point = 4 * cfg.d + 8 * cfg.L          # sketch kernel: read the point, write its L keys
+        sketch_avg_ms = sketch_ms / max(1, sketch_n)
+        achieved = bytes_per_point * n_local / (sketch_avg_ms * 1e-3) / 1e9 if sketch_avg_ms > 0 else None
+        roof = {"kernel": "sketch", "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "peak_kind": peak_kind,
+                "unit": "GB/s", "frac": (achieved / hbm_peak) if achieved else None,
+                "bytes_per_point": bytes_per_point, "traffic": ncu_traffic(cfg.name, scheme),
+                "avg_launch_ms": sketch_avg_ms}
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         rows = min(cfg.n, cpu_sample_rows(cfg))
@@ -339,11 +374,7 @@ def run_ours(args):
         "config": {"workload": f"{cfg.name}:{scheme}", "n": cfg.n, "d": cfg.d, "m": cfg.m, "L": cfg.L,
                    "K": cfg.K, "w": cfg.w, "queries_per_step": NQ, "parallelism": f"points sharded x{world}",
                    "l2": "inputs (%.2f GB) larger than L2; no flush" % (cfg.n * cfg.d * 4 / 1e9)},
-        "roofline": {"kernel": "sketch", "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
-                     "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": (achieved / hbm_peak) if achieved else None,
-                     "bytes_per_point": bytes_per_point, "traffic": traffic,
-                     "avg_launch_ms": sketch_avg_ms},
+        "roofline": roof,
         "kernel_ms_per_step": kernel_ms,
         "cpu_baseline": cpu,
         "e2e": e2e,

@@ -560,9 +560,10 @@ static lsh_status hash_impl(const lsh_handle* H, const float* X, int64_t n, int6
             const int64_t rows = std::min<int64_t>(n, (int64_t)dense_tc_rows_per_batch(H->d_pad));
             uint16_t* A = nullptr;
             CK(cudaMallocAsync((void**)&A, sizeof(uint16_t) * (size_t)rows * 3 * H->d_pad, s));
-            timing_begin("dense_gemm", s);
+            const std::string gname = std::string(tname) == "sketch" ? "dense_gemm" : "dense_gemm_query";
+            timing_begin(gname.c_str(), s);
             e = launch_dense_tc(X, n, ld, (int)p.d, H->d_Rpad, p.m, H->d_pad, A, rows, Y, s);
-            timing_end("dense_gemm", s);
+            timing_end(gname.c_str(), s);
             CK(cudaFreeAsync(A, s));
         }
         if (e != cudaSuccess) return cuda_fail(e, "dense_gemm");

@@ -24,7 +24,7 @@ constexpr int kTile = 4096;        // items per radix tile
 constexpr int kRT = 256;           // threads per radix block
 constexpr int kRounds = kTile / kRT;
 constexpr int kSegWin = 2048;      // positions owned by one segment-sort block
-constexpr int kSegCap = 256;       // longest segment sorted by the windowed kernel
+constexpr int kSegCap = 64;        // longest segment sorted by the windowed kernel (O(s^2) ranks)
 constexpr int kSegBig = 8192;      // CTA bitonic capacity in shared memory
 
 size_t group_tiles(int64_t n) { return (size_t)((n + kTile - 1) / kTile); }
@@ -273,8 +273,14 @@ __global__ void __launch_bounds__(256) segsort_window(uint64_t* __restrict__ key
         const bool beyond = (e == len) && (w0 + len < n) && (k[w0 + len] >> pre_sh) == pre;
         if (beyond || e - h > kSegCap) {
             if (li == h) {                                   // the head reports the long segment once
-                int64_t ge = w0 + e;
-                while (ge < n && (k[ge] >> pre_sh) == pre) ++ge;
+                // end of the prefix run: keys are sorted by prefix, so binary search
+                int64_t a = w0 + e, b = n;
+                while (a < b) {
+                    const int64_t mid = (a + b) >> 1;
+                    if ((k[mid] >> pre_sh) == pre) a = mid + 1;
+                    else b = mid;
+                }
+                const int64_t ge = a;
                 const uint32_t slot = atomicAdd(overflow, 1u);
                 if ((int)slot < cap) {
                     overflow[1 + 3 * slot] = (uint32_t)t;
@@ -326,11 +332,110 @@ __device__ void ascending_network(int64_t len, KeyAt less_at, Swap swap_at, bool
     }
 }
 
-__global__ void __launch_bounds__(1024) segsort_big(uint64_t* __restrict__ keys, uint32_t* __restrict__ ids, int64_t n,
-                                                    const uint32_t* overflow, int cap, int* flags) {
+// Long equal-prefix segment (many equal keys, e.g. duplicate points or empty codes):
+// one CTA runs a stable LSD radix sort of the segment on the key bits below the
+// common prefix (8-bit digits, digits that are constant over the segment are
+// skipped), ping-ponging with the free scratch buffers.  Items arrive id-ascending
+// and every pass is stable, so the result is the (key, id) order.
+__device__ void cta_radix_segment(uint64_t* k, uint32_t* d, uint64_t* k2, uint32_t* d2, int64_t len, int low_bits,
+                                  uint32_t* s_cnt, uint32_t* s_wcnt, uint32_t* s_woff, uint64_t* s_red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    // which digits vary across the segment?
+    uint64_t orv = 0, andv = ~0ull;
+    for (int64_t a = threadIdx.x; a < len; a += blockDim.x) {
+        orv |= k[a];
+        andv &= k[a];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        orv |= __shfl_xor_sync(0xffffffffu, orv, o);
+        andv &= __shfl_xor_sync(0xffffffffu, andv, o);
+    }
+    if (lane == 0) {
+        s_red[2 * warp] = orv;
+        s_red[2 * warp + 1] = andv;
+    }
+    __syncthreads();
+    orv = 0;
+    andv = ~0ull;
+    for (int w = 0; w < nw; ++w) {
+        orv |= s_red[2 * w];
+        andv &= s_red[2 * w + 1];
+    }
+    const uint64_t varying = orv ^ andv;
+    __syncthreads();
+    uint64_t *src_k = k, *dst_k = k2;
+    uint32_t *src_d = d, *dst_d = d2;
+    for (int sh = 0; sh < low_bits; sh += 8) {
+        if (((varying >> sh) & 255u) == 0) continue;
+        // histogram
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) s_cnt[i] = 0;
+        __syncthreads();
+        for (int64_t a = threadIdx.x; a < len; a += blockDim.x) atomicAdd(&s_cnt[(src_k[a] >> sh) & 255u], 1u);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t acc = 0;
+            for (int i = 0; i < 256; ++i) {
+                const uint32_t c = s_cnt[i];
+                s_cnt[i] = acc;
+                acc += c;
+            }
+        }
+        __syncthreads();
+        // stable scatter in rounds of blockDim items
+        for (int64_t base = 0; base < len; base += blockDim.x) {
+            const int64_t a = base + threadIdx.x;
+            const bool valid = a < len;
+            const uint64_t key = valid ? src_k[a] : 0;
+            const uint32_t id = valid ? src_d[a] : 0;
+            const uint32_t dg = valid ? (uint32_t)(key >> sh) & 255u : 256u;
+            const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+            const uint32_t rank = __popc(peers & lanemask_lt());
+            for (int i = threadIdx.x; i < nw * 256; i += blockDim.x) s_wcnt[i] = 0;
+            __syncthreads();
+            if (valid && rank == 0) s_wcnt[warp * 256 + dg] = __popc(peers);
+            __syncthreads();
+            for (int dd = threadIdx.x; dd < 256; dd += blockDim.x) {
+                uint32_t acc = s_cnt[dd];
+                for (int w = 0; w < nw; ++w) {
+                    s_woff[w * 256 + dd] = acc;
+                    acc += s_wcnt[w * 256 + dd];
+                }
+                s_cnt[dd] = acc;
+            }
+            __syncthreads();
+            if (valid) {
+                const uint32_t pos = s_woff[warp * 256 + dg] + rank;
+                dst_k[pos] = key;
+                dst_d[pos] = id;
+            }
+            __syncthreads();
+        }
+        uint64_t* tk = src_k;
+        src_k = dst_k;
+        dst_k = tk;
+        uint32_t* td = src_d;
+        src_d = dst_d;
+        dst_d = td;
+        __threadfence_block();
+        __syncthreads();
+    }
+    if (src_k != k) {  // odd number of passes: copy back
+        for (int64_t a = threadIdx.x; a < len; a += blockDim.x) {
+            k[a] = src_k[a];
+            d[a] = src_d[a];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(1024) segsort_big(uint64_t* __restrict__ keys, uint32_t* __restrict__ ids,
+                                                    uint64_t* __restrict__ scratch_k, uint32_t* __restrict__ scratch_d,
+                                                    int64_t n, int low_bits, const uint32_t* overflow, int cap,
+                                                    int* flags) {
     extern __shared__ __align__(16) unsigned char sm[];
     uint64_t* sk = reinterpret_cast<uint64_t*>(sm);
     uint32_t* si = reinterpret_cast<uint32_t*>(sm + kSegBig * sizeof(uint64_t));
+    __shared__ uint32_t s_cnt[256];
+    __shared__ uint64_t s_red[64];
     const uint32_t count = min(overflow[0], (uint32_t)cap);
     if (blockIdx.x == 0 && threadIdx.x == 0 && overflow[0] > (uint32_t)cap) atomicOr(flags, 4);
     for (uint32_t e = blockIdx.x; e < count; e += gridDim.x) {
@@ -339,32 +444,118 @@ __global__ void __launch_bounds__(1024) segsort_big(uint64_t* __restrict__ keys,
         uint64_t* k = keys + (int64_t)t * n + lo;
         uint32_t* d = ids + (int64_t)t * n + lo;
         const int64_t len = hi - lo;
-        if (len <= kSegBig) {
+        {   // all keys equal (repeated code tuples): already in id order
+            __shared__ int s_neq;
+            if (threadIdx.x == 0) s_neq = 0;
+            __syncthreads();
+            const uint64_t k0 = k[0];
+            int neq = 0;
+            for (int64_t a = threadIdx.x; a < len && !neq; a += blockDim.x) neq = k[a] != k0;
+            if (neq) s_neq = 1;
+            __syncthreads();
+            const int any = s_neq;
+            __syncthreads();
+            if (!any) continue;
+        }
+        // the per-warp count tables live in the dynamic smem area (unused by the partition)
+        uint32_t* s_wcnt = reinterpret_cast<uint32_t*>(sm);
+        uint32_t* s_woff = s_wcnt + 32 * 256;
+        uint64_t* k2 = scratch_k + (int64_t)t * n + lo;
+        uint32_t* d2 = scratch_d + (int64_t)t * n + lo;
+        // Long segments are dominated by repeated keys (duplicate points, empty codes):
+        // stable 3-way partition around the middle item's key first; the "equal" part is
+        // already in id order, only the rest needs sorting.
+        const uint64_t pivot = k[len / 2];
+        __shared__ uint32_t s_lt, s_eq;
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        if (threadIdx.x == 0) {
+            s_lt = 0;
+            s_eq = 0;
+        }
+        __syncthreads();
+        {
+            uint32_t lt = 0, eq = 0;
             for (int64_t a = threadIdx.x; a < len; a += blockDim.x) {
-                sk[a] = k[a];
-                si[a] = d[a];
+                lt += k[a] < pivot;
+                eq += k[a] == pivot;
+            }
+            atomicAdd(&s_lt, lt);
+            atomicAdd(&s_eq, eq);
+        }
+        __syncthreads();
+        const uint32_t nlt = s_lt, neq = s_eq;
+        uint32_t base0 = 0, base1 = nlt, base2 = nlt + neq;
+        for (int64_t b0 = 0; b0 < len; b0 += blockDim.x) {
+            const int64_t a = b0 + threadIdx.x;
+            const bool valid = a < len;
+            const uint64_t key = valid ? k[a] : 0;
+            const uint32_t cls = !valid ? 3u : (key < pivot ? 0u : (key == pivot ? 1u : 2u));
+            const uint32_t m0 = __ballot_sync(0xffffffffu, cls == 0), m1 = __ballot_sync(0xffffffffu, cls == 1),
+                           m2 = __ballot_sync(0xffffffffu, cls == 2);
+            if (lane == 0) {
+                s_wcnt[warp * 3 + 0] = __popc(m0);
+                s_wcnt[warp * 3 + 1] = __popc(m1);
+                s_wcnt[warp * 3 + 2] = __popc(m2);
             }
             __syncthreads();
-            ascending_network(
-                len, [&](int64_t x, int64_t y) { return kless(sk[x], si[x], sk[y], si[y]); },
-                [&](int64_t x, int64_t y) {
-                    const uint64_t tk = sk[x]; sk[x] = sk[y]; sk[y] = tk;
-                    const uint32_t ti = si[x]; si[x] = si[y]; si[y] = ti;
-                },
-                true);
-            for (int64_t a = threadIdx.x; a < len; a += blockDim.x) {
-                k[a] = sk[a];
-                d[a] = si[a];
+            uint32_t pre0 = base0, pre1 = base1, pre2 = base2;
+            for (int w = 0; w < warp; ++w) {
+                pre0 += s_wcnt[w * 3];
+                pre1 += s_wcnt[w * 3 + 1];
+                pre2 += s_wcnt[w * 3 + 2];
             }
-        } else {
-            // long segment (many equal keys): the same network in place in global memory
-            ascending_network(
-                len, [&](int64_t x, int64_t y) { return kless(k[x], d[x], k[y], d[y]); },
-                [&](int64_t x, int64_t y) {
-                    const uint64_t tk = k[x]; k[x] = k[y]; k[y] = tk;
-                    const uint32_t ti = d[x]; d[x] = d[y]; d[y] = ti;
-                },
-                false);
+            const uint32_t lm = (1u << lane) - 1u;
+            if (valid) {
+                const uint32_t pos = cls == 0 ? pre0 + __popc(m0 & lm) : cls == 1 ? pre1 + __popc(m1 & lm)
+                                                                                  : pre2 + __popc(m2 & lm);
+                k2[pos] = key;
+                d2[pos] = d[a];
+            }
+            for (int w = 0; w < nw; ++w) {
+                base0 += s_wcnt[w * 3];
+                base1 += s_wcnt[w * 3 + 1];
+                base2 += s_wcnt[w * 3 + 2];
+            }
+            __syncthreads();
+        }
+        __threadfence_block();
+        __syncthreads();
+        for (int64_t a = threadIdx.x; a < len; a += blockDim.x) {
+            k[a] = k2[a];
+            d[a] = d2[a];
+        }
+        __threadfence_block();
+        __syncthreads();
+        const int64_t ngt = len - nlt - neq;
+        const int64_t part_lo[2] = {0, (int64_t)nlt + neq};
+        const int64_t part_len[2] = {(int64_t)nlt, ngt};
+        for (int q = 0; q < 2; ++q) {
+            const int64_t plen = part_len[q];
+            if (plen <= 1) continue;
+            uint64_t* pk = k + part_lo[q];
+            uint32_t* pd = d + part_lo[q];
+            if (plen <= kSegBig) {
+                for (int64_t a = threadIdx.x; a < plen; a += blockDim.x) {
+                    sk[a] = pk[a];
+                    si[a] = pd[a];
+                }
+                __syncthreads();
+                ascending_network(
+                    plen, [&](int64_t x, int64_t y) { return kless(sk[x], si[x], sk[y], si[y]); },
+                    [&](int64_t x, int64_t y) {
+                        const uint64_t tk = sk[x]; sk[x] = sk[y]; sk[y] = tk;
+                        const uint32_t ti = si[x]; si[x] = si[y]; si[y] = ti;
+                    },
+                    true);
+                for (int64_t a = threadIdx.x; a < plen; a += blockDim.x) {
+                    pk[a] = sk[a];
+                    pd[a] = si[a];
+                }
+                __syncthreads();
+            } else {
+                cta_radix_segment(pk, pd, k2 + part_lo[q], d2 + part_lo[q], plen, low_bits, s_cnt, s_wcnt, s_woff,
+                                  s_red);
+            }
         }
         __syncthreads();
     }
@@ -492,11 +683,15 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
         const dim3 gw((unsigned)((n + kSegWin - 1) / kSegWin), L);
         segsort_window<<<gw, 256, 0, s>>>(sorted, out.ids, n, W - 16, sc.overflow, sc.overflow_cap);
         count_launch();
+        timing_end("segsort", s);
+        timing_begin("segsort_long", s);
         const size_t smem = kSegBig * (sizeof(uint64_t) + sizeof(uint32_t));
         cudaFuncSetAttribute(segsort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        segsort_big<<<148, 1024, smem, s>>>(sorted, out.ids, n, sc.overflow, sc.overflow_cap, flags);
+        // scratch for long segments: the pass-0 buffers are free once pass 1 has run
+        segsort_big<<<148, 1024, smem, s>>>(sorted, out.ids, sc.keys_a, sc.ids_a, n, W - 16, sc.overflow,
+                                            sc.overflow_cap, flags);
         count_launch();
-        timing_end("segsort", s);
+        timing_end("segsort_long", s);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     timing_begin("rle", s);

@@ -304,3 +304,19 @@ def test_dense_tensor_core_shapes(m, L, K):
         p = lsh.Params(scheme, d=300, m=m, L=L, K=K, w=2.0, seed=9)
         X = synth.gaussian_rows_like(333, 300, 4, device="cuda")
         _compare(p, X, X.cpu().numpy())
+
+
+def test_group_long_equal_prefix_segments():
+    """Many keys sharing their top 16 bits (long segments -> CTA radix path), ties by id."""
+    p = lsh.Params("CS_E2LSH", d=64, m=32, L=2, K=16, w=4.0, seed=0)
+    h = _handle(p)
+    g = np.random.default_rng(3)
+    n = 50000
+    keys = g.integers(0, 2 ** 62, (2, n), dtype=np.int64).astype(np.uint64)
+    pref = np.uint64(0xABCD) << np.uint64(48)
+    keys[0, :30000] = pref | g.integers(0, 50, 30000).astype(np.uint64)          # 50 distinct low parts
+    keys[1, 10000:20000] = pref | (g.integers(0, 3, 10000).astype(np.uint64) << np.uint64(40))
+    keys[1, 30000:39000] = keys[1, 30000]                                             # all equal
+    idx = h.group_keys(torch.from_numpy(keys.view(np.int64)).cuda().view(torch.uint64), id_base=5)
+    _check_index(idx, lsh.group(keys, id_base=5), 2)
+    h.check()
