@@ -298,6 +298,75 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t* bpc = s_bp + (SINGLE ? 0 : c * (m + 1));
         const uint8_t* cntc = s_cnt + (SINGLE ? 0 : (size_t)c * m);
         const uint32_t cbase = SINGLE ? 0u : (uint32_t)(c * Q);
+        if constexpr (KT > 0 && SINGLE) {
+            // Phased table loop (hot path): all 2*K loads first (branch-free for bins with
+            // <= 2 coordinates), rare fix-ups for fuller bins, then discretise + key.
+            for (int t = warp; t < L; t += kWarps) {
+                const float* p = T + bpc[t * K] * 33 + lane;
+                uint32_t cw[KT / 4];
+                const uint32_t* cp = reinterpret_cast<const uint32_t*>(cntc + t * KT);
+#pragma unroll
+                for (int i = 0; i < KT / 4; ++i) cw[i] = cp[i];
+                float acc[KT];
+                uint32_t big = 0;
+                {
+                    const float* pp = p;
+#pragma unroll
+                    for (int kk = 0; kk < KT; ++kk) {
+                        const uint32_t cnt = (cw[kk >> 2] >> (8 * (kk & 3))) & 255u;
+                        const float v0 = pp[0];
+                        const float v1 = pp[33];
+                        float a = cnt > 0 ? 0.0f + v0 : 0.0f;
+                        a = cnt > 1 ? a + v1 : a;
+                        acc[kk] = a;
+                        big |= (cnt > 2 ? 1u : 0u) << kk;
+                        pp += cnt * 33;
+                    }
+                }
+                if (big) {
+                    const float* pp = p;
+#pragma unroll
+                    for (int kk = 0; kk < KT; ++kk) {
+                        const uint32_t cnt = (cw[kk >> 2] >> (8 * (kk & 3))) & 255u;
+                        if (cnt > 2)
+                            for (uint32_t j = 2; j < cnt; ++j) acc[kk] += pp[j * 33];
+                        pp += cnt * 33;
+                    }
+                }
+                uint64_t f = E2 ? LSHB_FNV_OFFSET : 0ull;
+                if constexpr (E2) {
+                    float qmax = 0.f;
+                    const float4* co = reinterpret_cast<const float4*>(s_coff + t * KT);
+#pragma unroll
+                    for (int k4 = 0; k4 < KT / 4; ++k4) {
+                        const float4 c4 = co[k4];
+                        const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const float q = fmaf(acc[4 * k4 + j], cs, cc[j]);
+                            qmax = fmax_nan_abs(qmax, q);
+                            const int32_t z = __float_as_int(__fadd_rd(q, 12582912.0f)) - 0x4B400000;
+                            f = (f ^ (uint64_t)(uint32_t)z) * LSHB_FNV_PRIME;
+                        }
+                    }
+                    if (!(qmax < 4194304.0f)) {
+                        f = LSHB_FNV_OFFSET;
+#pragma unroll
+                        for (int kk = 0; kk < KT; ++kk) {
+                            const int32_t z = floor_code(fmaf(acc[kk], cs, s_coff[t * KT + kk]), dz.flags);
+                            f = (f ^ (uint64_t)(uint32_t)z) * LSHB_FNV_PRIME;
+                        }
+                    }
+                    f = fmix64_dev(f);
+                } else {
+                    uint32_t sb = 0;
+#pragma unroll
+                    for (int kk = 0; kk < KT; ++kk) sb |= (acc[kk] > 0.0f ? 1u : 0u) << kk;
+                    f = sb;
+                }
+                if (valid && out.keys) out.keys[(int64_t)t * n + row] = f;
+            }
+        } else
         for (int t = warp; t < L; t += kWarps) {
             const float* p = T + (bpc[t * K] - cbase) * 33 + lane;
             uint64_t f = E2 ? LSHB_FNV_OFFSET : 0ull;
