@@ -260,6 +260,8 @@ struct lsh_handle {
     uint16_t* d_entries = nullptr;
     uint32_t* d_binptr = nullptr;
     uint32_t* d_signs = nullptr;
+    uint32_t* d_pairs = nullptr;
+    uint32_t* d_bigmask = nullptr;
     float* d_coff = nullptr;
     uint16_t* d_R = nullptr;
     uint16_t* d_Rpad = nullptr;  // bf16 [m][d_pad], d_pad = roundup(d, 64): tensor-core B operand
@@ -404,30 +406,43 @@ static lsh_status build_plan(lsh_handle* H) {
     const int d = (int)p->d, m = p->m;
     const int vpt = d <= 64 ? 1 : (d <= 256 ? 4 : 16);
     const int Q = 64 * vpt;
-    if (d > Q || sketch_smem_bytes(Q, m, d, 1) > 232448) return build_chunked_plan(H, bin, sgn);
-    const int nchunks = 1;
-    std::vector<uint32_t> bin_ptr((size_t)nchunks * (m + 1), 0);
-    std::vector<uint16_t> pos(d);
+    if (d > Q || sketch_smem_bytes(Q, m, d, p->L) > 232448) return build_chunked_plan(H, bin, sgn);
+    // single resident tile: bins in bin-sorted order (ascending coordinate inside a bin);
+    // ent = the staged tile's word offset of each coordinate (transposed layout of sketch.cu)
+    std::vector<uint32_t> bin_ptr(m + 1, 0);
+    std::vector<uint16_t> ent(d);
     std::vector<uint32_t> sign_bits((d + 31) / 32, 0);
     for (int j = 0; j < d; ++j)
         if (sgn[j] < 0) sign_bits[j >> 5] |= 1u << (j & 31);
+    for (int j = 0; j < d; ++j) bin_ptr[bin[j] + 1]++;
+    for (int l = 0; l < m; ++l) bin_ptr[l + 1] += bin_ptr[l];
     {
-        std::vector<uint32_t> cnt(m + 1, 0);
-        for (int j = 0; j < d; ++j) cnt[bin[j] + 1]++;
-        for (int l = 0; l < m; ++l) cnt[l + 1] += cnt[l];
-        for (int l = 0; l <= m; ++l) bin_ptr[l] = cnt[l];
-        std::vector<uint32_t> cur(cnt.begin(), cnt.end() - 1);
-        for (int j = 0; j < d; ++j) pos[j] = (uint16_t)(cur[bin[j]]++);  // ascending j inside each bin
+        std::vector<uint32_t> cur(bin_ptr.begin(), bin_ptr.end() - 1);
+        for (int j = 0; j < d; ++j) ent[cur[bin[j]]++] = (uint16_t)((j >> 2) * 129 + (j & 3) * 32);
+    }
+    const uint32_t ZW = (uint32_t)(Q / 4) * 129u;
+    int max_cnt = 0;
+    std::vector<uint32_t> pairs(m), bigmask(p->L, 0);
+    for (int l = 0; l < m; ++l) {
+        const uint32_t c = bin_ptr[l + 1] - bin_ptr[l];
+        max_cnt = std::max(max_cnt, (int)c);
+        const uint32_t a = c >= 1 ? ent[bin_ptr[l]] : ZW;
+        const uint32_t b = c >= 2 ? ent[bin_ptr[l] + 1] : ZW;
+        pairs[l] = a | (b << 16);
+        if (c > 2 && p->K <= 32) bigmask[l / p->K] |= 1u << (l % p->K);
     }
     CK(cudaMalloc(&H->d_entries, sizeof(uint16_t) * std::max(1, d)));
     CK(cudaMalloc(&H->d_binptr, sizeof(uint32_t) * bin_ptr.size()));
     CK(cudaMalloc(&H->d_signs, sizeof(uint32_t) * sign_bits.size()));
-    CK(cudaMemcpy(H->d_entries, pos.data(), sizeof(uint16_t) * d, cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&H->d_pairs, sizeof(uint32_t) * m));
+    CK(cudaMalloc(&H->d_bigmask, sizeof(uint32_t) * p->L));
+    CK(cudaMemcpy(H->d_entries, ent.data(), sizeof(uint16_t) * d, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(H->d_binptr, bin_ptr.data(), sizeof(uint32_t) * bin_ptr.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(H->d_signs, sign_bits.data(), sizeof(uint32_t) * sign_bits.size(), cudaMemcpyHostToDevice));
-    int max_cnt = 0;
-    for (int l = 0; l < m; ++l) max_cnt = std::max(max_cnt, (int)(bin_ptr[l + 1] - bin_ptr[l]));
-    H->plan = SketchPlanDev{d, m, p->L, p->K, Q, vpt, nchunks, max_cnt, H->d_entries, H->d_binptr, H->d_signs};
+    CK(cudaMemcpy(H->d_pairs, pairs.data(), sizeof(uint32_t) * m, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(H->d_bigmask, bigmask.data(), sizeof(uint32_t) * p->L, cudaMemcpyHostToDevice));
+    H->plan = SketchPlanDev{d, m, p->L, p->K, Q, vpt, 1, max_cnt, H->d_entries, H->d_binptr, H->d_signs,
+                            H->d_pairs, H->d_bigmask};
     return LSH_OK;
 }
 
@@ -437,6 +452,8 @@ static void free_handle(lsh_handle* H) {
     cudaFree(H->d_binptr);
     cudaFree(H->d_cplan_mem);
     cudaFree(H->d_signs);
+    cudaFree(H->d_pairs);
+    cudaFree(H->d_bigmask);
     cudaFree(H->d_coff);
     cudaFree(H->d_R);
     cudaFree(H->d_Rpad);

@@ -24,9 +24,12 @@ struct SketchPlanDev {
     int vpt;          // float4 registers per thread (template selector: 1, 4, 16)
     int nchunks;
     int max_cnt;      // largest number of coordinates of one bin inside one chunk
-    const uint16_t* pos;        // [d] rank of coordinate j in its chunk's bin-sorted order (ascending j in a bin)
+    const uint16_t* pos;        // [d] staged-tile word offset of the coordinate at each bin-sorted index
     const uint32_t* bin_ptr;    // [nchunks][m+1] absolute index (chunk start + rank) where each bin starts
     const uint32_t* sign_bits;  // [ceil(d/32)] bit j set = sign(j) = -1 (applied while staging)
+    const uint32_t* pairs;      // [m] per bin: word offsets (pos*33) of its first two staged coordinates,
+                                //     lo 16 bits / hi 16 bits; missing ones point at the zero slot Q
+    const uint32_t* bigmask;    // [L] bit k set: bin k of table t has more than 2 coordinates
 };
 
 // Chunked plan (sketch_chunked.cu): tables in groups, per group the coordinates
@@ -70,7 +73,7 @@ struct HashOut {
 // Launchers (return cudaError_t of the launch).
 cudaError_t launch_sketch(const SketchPlanDev& plan, const DiscretizeDev& disc, const float* X, int64_t n,
                           int64_t ld, HashOut out, int num_sms, cudaStream_t s);
-size_t sketch_smem_bytes(int Q, int m, int d, int nchunks);
+size_t sketch_smem_bytes(int Q, int m, int d, int L);
 cudaError_t launch_sketch_chunked(const ChunkedPlanDev& plan, const DiscretizeDev& disc, const float* X, int64_t n,
                                   int64_t ld, HashOut out, int num_sms, cudaStream_t s);
 size_t chunked_smem_bytes(int m, int gbins);
