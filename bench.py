@@ -273,7 +273,7 @@ def run_ours(args):
     ms_local = ev0.elapsed_time(ev1) / args.steps
     sketch_ms, sketch_n = pk.timing_get("sketch")
     kernel_ms = {k: pk.timing_get(k)[0] / max(1, args.steps) for k in
-                 ("sketch", "sketch_query", "radix_upsweep", "radix_scan", "radix_downsweep", "segsort", "segsort_long", "rle", "lookup", "counts",
+                 ("sketch", "sketch_query", "group_hist", "group_scan", "group_scatter", "group_sort", "lookup", "counts",
                   "global_offsets", "dense_gemm", "keys_from_proj")}
     keep.clear()
     t = torch.tensor([ms_local], device=dev)

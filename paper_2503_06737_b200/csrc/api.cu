@@ -641,34 +641,47 @@ static lsh_status alloc_index(const lsh_handle* H, int64_t n, cudaStream_t s, ls
     return LSH_OK;
 }
 
-static lsh_status group_impl(const lsh_handle* H, const uint64_t* keys, uint64_t* keys_scratch_b, int64_t n,
+static lsh_status group_impl(const lsh_handle* H, const uint64_t* keys, uint64_t* keys_scratch, int64_t n,
                              int64_t id_base, lsh_index* I, cudaStream_t s) {
+    // keys_scratch: a dead [L][n] u64 buffer (the hashed keys of lsh_build_index, fully
+    // consumed by the L1 scatter before the per-bin kernel runs) reused as [L][2n] u32
+    // permutation scratch; nullptr = allocate it.
     const int L = H->p.L;
     GroupScratch sc{};
-    const size_t T = group_tiles(n);
+    const size_t nb1 = (size_t)group_bins(n, H->key_width);
     const size_t b_keys = sizeof(uint64_t) * (size_t)L * n;
-    sc.overflow_cap = 1 << 16;
-    const size_t b_hist = sizeof(uint32_t) * (size_t)L * 256 * std::max<size_t>(T, 1);
-    const size_t b_aux = sizeof(uint32_t) * (size_t)L * (T + 1);
-    const size_t b_ovf = sizeof(uint32_t) * (1 + 3 * (size_t)sc.overflow_cap);
     const size_t b_ids = sizeof(uint32_t) * (size_t)L * n;
-    const bool own_b = (keys_scratch_b == nullptr);
-    const size_t total = b_keys * (own_b ? 2 : 1) + b_ids + b_hist + b_aux + b_ovf + 256;
+    const size_t b_hist = sizeof(uint32_t) * (size_t)L * std::max<size_t>(group_hist_words(n, H->key_width), 1);
+    const size_t b_tot = sizeof(uint32_t) * (size_t)L * nb1;
+    const size_t b_bs = sizeof(uint32_t) * (size_t)L * (nb1 + 1);
+    const size_t b_st = sizeof(unsigned long long) * (size_t)L * (size_t)std::max(group_chunks(n), 1);
+    const bool own_perm = (keys_scratch == nullptr);
+    const size_t b_perm = own_perm ? b_keys : 0;
+    const size_t b_vm = sizeof(unsigned long long) * 2 * (size_t)L;
+    const size_t b_spec = group_spec_bytes() * 2 * (size_t)L;
+    const size_t b_cb = sizeof(uint32_t) * (size_t)L * ((size_t)std::max(group_chunks(n), 1) + 1);
     void* mem = nullptr;
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    const size_t total = al(b_keys) + al(b_ids) + al(b_hist) + al(b_tot) + al(b_bs) + al(b_st) + al(b_perm) + al(b_vm) +
+                         al(b_spec) + al(b_cb);
     if (n > 0) CK(cudaMallocAsync(&mem, total, s));
     char* p = (char*)mem;
     auto take = [&](size_t b) {
         char* r = p;
-        p += (b + 127) / 128 * 128;
+        p += al(b);
         return r;
     };
     if (n > 0) {
         sc.keys_a = (uint64_t*)take(b_keys);
-        sc.keys_b = own_b ? (uint64_t*)take(b_keys) : keys_scratch_b;
         sc.ids_a = (uint32_t*)take(b_ids);
         sc.hist = (uint32_t*)take(b_hist);
-        sc.tile_aux = (uint32_t*)take(b_aux);
-        sc.overflow = (uint32_t*)take(b_ovf);
+        sc.tot = (uint32_t*)take(b_tot);
+        sc.binstart = (uint32_t*)take(b_bs);
+        sc.state = (unsigned long long*)take(b_st);
+        sc.perm = own_perm ? (uint32_t*)take(b_perm) : (uint32_t*)keys_scratch;
+        sc.vmask = (unsigned long long*)take(b_vm);
+        sc.spec = take(b_spec);
+        sc.chunkbin = (uint32_t*)take(b_cb);
     }
     cudaError_t e = launch_group(keys, n, L, (uint32_t)id_base, H->key_width, sc, I->dev, H->d_flags, s);
     if (e != cudaSuccess) return cuda_fail(e, "group");

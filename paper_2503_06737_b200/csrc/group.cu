@@ -6,13 +6,21 @@
 // Output order is canonical (reading B11): per table, ids sorted by (key, id),
 // i.e. buckets by ascending unsigned key, ids ascending inside a bucket.
 //
-//   1. stable LSD counting-sort passes on the top 16 significant key bits
-//      (8-bit digits; warp-level match_any ranking keeps each pass stable, so
-//      ids stay ascending inside equal digits),
-//   2. if keys are wider than 16 bits (E2LSH fingerprints, SRP with K > 16):
-//      stable sort of each equal-top-16 segment by the full key (segments are
-//      ~n/65536 long for fingerprints; long ones go to a CTA-level bitonic sort),
-//   3. run-length encoding -> ukeys / offs / nb.
+// B200 design (two passes over the keys after the histogram):
+//   L1  one stable MSD counting scatter of every table on its top B1 key bits
+//       (B1 = 1..11 chosen so bins average <= 2048 items).  The destination of
+//       one table (12 B x n) stays resident in the 126 MB L2 while the grid
+//       works on that table, so the scattered runs merge in L2 before they
+//       reach HBM.  Stability comes from warp-private match_any ranking.
+//   L2  one CTA per (bin, table): the bin is loaded into shared memory and
+//       sorted there by the next 16 key bits (two stable 8-bit passes on a
+//       16-bit permutation), equal-prefix segments are finished by O(s) ranks
+//       (long ones by further passes), then run-length encoded.  The bucket
+//       numbering across bins is a decoupled look-back (chained) scan, so ids,
+//       ukeys and offs are written once, compacted, in the same kernel.
+//   Bins larger than shared memory (skewed codes: many equal keys) take the
+//   same algorithm on global memory: a stable 3-way split around a dominant
+//   key, then stable 8-bit passes over the varying digits only.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -20,14 +28,31 @@
 
 namespace lshb {
 
-constexpr int kTile = 4096;        // items per radix tile
-constexpr int kRT = 256;           // threads per radix block
-constexpr int kRounds = kTile / kRT;
-constexpr int kSegWin = 2048;      // positions owned by one segment-sort block
-constexpr int kSegCap = 64;        // longest segment sorted by the windowed kernel (O(s^2) ranks)
-constexpr int kSegBig = 8192;      // CTA bitonic capacity in shared memory
+constexpr int kG1Tile = 4096;                   // items per L1 tile
+constexpr int kG1Threads = 256;
+constexpr int kG1Warps = kG1Threads / 32;       // 8
+constexpr int kG1PerWarp = kG1Tile / kG1Warps;  // 512 consecutive items per warp
+constexpr int kG1Rounds = kG1PerWarp / 32;      // 16
+constexpr int kG2Threads = 512;
+constexpr int kG2Warps = kG2Threads / 32;       // 16
+constexpr int kG2Cap = 4096;                    // bin items sorted in shared memory
+constexpr int kG2Span = kG2Cap / 2;            // L2 chunk: bins starting inside a span of this many items
+constexpr int kG2Seg = 64;                      // longest equal-prefix segment finished by O(s) ranks
+constexpr int kG2Long = kG2Cap / kG2Seg;        // long-segment list capacity
 
-size_t group_tiles(int64_t n) { return (size_t)((n + kTile - 1) / kTile); }
+size_t group_tiles(int64_t n) { return (size_t)((n + kG1Tile - 1) / kG1Tile); }
+
+// Narrow keys (SRP codes, K <= 22) are sorted completely by two stable LSD passes
+// over their varying bits (<= 11 each); wide keys (E2LSH fingerprints) by one MSD
+// pass + the per-chunk shared-memory sort.
+bool group_is_lsd(int W) { return W <= 22; }
+
+int group_l1_bits(int64_t n, int W) {
+    if (group_is_lsd(W)) return (W + 1) / 2;
+    int b = 1;
+    while (b < 11 && ((n + (1ll << b) - 1) >> b) > kG2Span / 2) ++b;
+    return b < W ? b : W;
+}
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t r;
@@ -35,210 +60,11 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     return r;
 }
 
-template <bool IMPLICIT_IDS>
-__global__ void __launch_bounds__(kRT) radix_upsweep(const uint64_t* __restrict__ keys, int64_t n, int sh,
-                                                     uint32_t* __restrict__ hist, int T) {
-    __shared__ uint32_t cnt[256];
-    const int t = blockIdx.y, tile = blockIdx.x;
-    cnt[threadIdx.x] = 0;
-    __syncthreads();
-    const uint64_t* kt = keys + (int64_t)t * n;
-    for (int r = 0; r < kRounds; ++r) {
-        const int64_t i = (int64_t)tile * kTile + r * kRT + threadIdx.x;
-        if (i < n) atomicAdd(&cnt[(kt[i] >> sh) & 255], 1u);
-    }
-    __syncthreads();
-    hist[((int64_t)t * 256 + threadIdx.x) * T + tile] = cnt[threadIdx.x];
-}
-
-// Exclusive scan of `len` uint32 values per table (row stride `stride`) in place;
-// writes the total to total_out[t] if non-null and also at a[len] if write_end.
-__global__ void __launch_bounds__(1024) scan_rows(uint32_t* a, int64_t len, int64_t stride, uint32_t* total_out,
-                                                  int write_end) {
-    __shared__ uint32_t wsum[32];
-    __shared__ uint32_t carry_s;
-    uint32_t* row = a + (int64_t)blockIdx.x * stride;
+// Exclusive block scan of one value per thread (NT threads); optional total.
+template <int NT>
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* ws, uint32_t* total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) carry_s = 0;
-    __syncthreads();
-    for (int64_t base = 0; base < len; base += 1024) {
-        const int64_t i = base + threadIdx.x;
-        const uint32_t v = i < len ? row[i] : 0u;
-        uint32_t x = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) wsum[warp] = x;
-        __syncthreads();
-        if (warp == 0) {
-            uint32_t w = wsum[lane];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-                if (lane >= o) w += y;
-            }
-            wsum[lane] = w;
-        }
-        __syncthreads();
-        const uint32_t carry = carry_s;
-        const uint32_t excl = carry + (warp ? wsum[warp - 1] : 0u) + x - v;
-        if (i < len) row[i] = excl;
-        __syncthreads();
-        if (threadIdx.x == 1023) carry_s = excl + v;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        if (total_out) total_out[blockIdx.x] = carry_s;
-        if (write_end) row[len] = carry_s;
-    }
-}
-
-// Stable scatter of one 4096-item tile by an 8-bit digit.  Warp w owns the tile's
-// items [512w, 512w+512) (coalesced 32-item rounds); a warp ranks its items with
-// match_any against its own running per-digit counters (no block barrier per
-// round), then one block-wide pass turns (digit, warp) counts into offsets.  Items
-// are placed in digit order in shared memory and written out so that consecutive
-// threads write consecutive addresses.  Order inside a digit = item order: stable.
-template <bool IMPLICIT_IDS>
-__global__ void __launch_bounds__(kRT) radix_downsweep(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ iin,
-                                                       uint64_t* __restrict__ kout, uint32_t* __restrict__ iout,
-                                                       int64_t n, int sh, const uint32_t* __restrict__ hist, int T,
-                                                       uint32_t id_base) {
-    constexpr int W = kRT / 32;             // warps
-    constexpr int PER_WARP = kTile / W;     // 512 items
-    constexpr int R = PER_WARP / 32;        // 16 rounds
-    __shared__ uint32_t wrun[W][256];       // per-warp running digit counts, then warp offsets
-    __shared__ uint32_t tile_off[256];
-    __shared__ uint32_t local_off[256];
-    __shared__ uint32_t ws[W];
-    extern __shared__ __align__(16) unsigned char dsm[];
-    uint64_t* sk = reinterpret_cast<uint64_t*>(dsm);                  // [kTile]
-    uint32_t* si = reinterpret_cast<uint32_t*>(dsm + kTile * 8);      // [kTile]
-    const int t = blockIdx.y, tile = blockIdx.x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int w = 0; w < W; ++w) wrun[w][threadIdx.x] = 0;
-    tile_off[threadIdx.x] = hist[((int64_t)t * 256 + threadIdx.x) * T + tile];
-    __syncthreads();
-    const int64_t tb = (int64_t)t * n;
-    const int64_t base = (int64_t)tile * kTile + warp * PER_WARP;
-    uint64_t key[R];
-    uint32_t id[R], slot[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const int64_t i = base + r * 32 + lane;
-        const bool valid = i < n;
-        key[r] = valid ? kin[tb + i] : ~0ull;
-        id[r] = valid ? (IMPLICIT_IDS ? id_base + (uint32_t)i : iin[tb + i]) : 0u;
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const int64_t i = base + r * 32 + lane;
-        const bool valid = i < n;
-        const uint32_t dg = valid ? ((uint32_t)(key[r] >> sh) & 255u) : 256u;
-        const uint32_t peers = __match_any_sync(0xffffffffu, dg);
-        const uint32_t rank = __popc(peers & lanemask_lt());
-        uint32_t before = 0;
-        if (valid) before = wrun[warp][dg];
-        __syncwarp();
-        if (valid && rank == 0) wrun[warp][dg] = before + __popc(peers);
-        __syncwarp();
-        slot[r] = valid ? (dg << 16) | (before + rank) : 0xffffffffu;
-    }
-    __syncthreads();
-    {   // per digit: exclusive prefix over warps, and the tile's digit totals
-        const int dd = threadIdx.x;
-        uint32_t acc = 0;
-#pragma unroll
-        for (int w = 0; w < W; ++w) {
-            const uint32_t c = wrun[w][dd];
-            wrun[w][dd] = acc;
-            acc += c;
-        }
-        // exclusive scan of totals across digits -> local_off
-        uint32_t x = acc;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) ws[warp] = x;
-        __syncthreads();
-        uint32_t pre = 0;
-        for (int w = 0; w < warp; ++w) pre += ws[w];
-        local_off[dd] = pre + x - acc;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        if (slot[r] != 0xffffffffu) {
-            const uint32_t dg = slot[r] >> 16;
-            const uint32_t p = local_off[dg] + wrun[warp][dg] + (slot[r] & 0xffffu);
-            sk[p] = key[r];
-            si[p] = id[r];
-        }
-    }
-    __syncthreads();
-    const int64_t cnt = min((int64_t)kTile, n - (int64_t)tile * kTile);
-    for (int p = threadIdx.x; p < cnt; p += kRT) {
-        const uint64_t k = sk[p];
-        const uint32_t dg = (uint32_t)(k >> sh) & 255u;
-        const uint32_t pos = tile_off[dg] + (p - local_off[dg]);
-        kout[tb + pos] = k;
-        iout[tb + pos] = si[p];
-    }
-}
-
-__device__ __forceinline__ bool kless(uint64_t ka, uint32_t ia, uint64_t kb, uint32_t ib) {
-    return ka < kb || (ka == kb && ia < ib);
-}
-
-// Segments of equal top-16 significant bits: stable sort by the full key.  One
-// block owns the segments whose head lies in its window of kSegWin positions and
-// loads the window plus kSegCap positions of look-ahead into shared memory.
-// Segment heads are found with one block scan; each item's rank inside its
-// segment is #{smaller keys} + #{equal keys before it} (items arrive id-ascending
-// inside a segment, so this is the stable order).  Longer segments go to the
-// overflow list (segsort_big).
-__global__ void __launch_bounds__(256) segsort_window(uint64_t* __restrict__ keys, uint32_t* __restrict__ ids, int64_t n,
-                                                      int pre_sh, uint32_t* overflow, int cap) {
-    constexpr int LEN = kSegWin + kSegCap;
-    constexpr int PER = (LEN + 255) / 256;
-    __shared__ uint64_t sk[LEN];
-    __shared__ uint32_t si[LEN];
-    __shared__ uint16_t seg_of[LEN];
-    __shared__ uint16_t seg_start[LEN + 1];
-    __shared__ uint32_t ws[8];
-    __shared__ int nseg_s;
-    const int t = blockIdx.y;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t w0 = (int64_t)blockIdx.x * kSegWin;
-    uint64_t* k = keys + (int64_t)t * n;
-    uint32_t* d = ids + (int64_t)t * n;
-    const int len = (int)min((int64_t)LEN, n - w0);
-    const int own = (int)min((int64_t)kSegWin, n - w0);
-    for (int a = threadIdx.x; a < len; a += blockDim.x) {
-        sk[a] = k[w0 + a];
-        si[a] = d[w0 + a];
-    }
-    const uint64_t prev_pre = w0 > 0 ? (k[w0 - 1] >> pre_sh) : ~0ull;
-    __syncthreads();
-    // head flags over my PER consecutive positions, block scan -> segment ids
-    const int a0 = threadIdx.x * PER;
-    uint32_t flags = 0, cntf = 0;
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-        const int a = a0 + q;
-        if (a < len) {
-            const uint64_t pr = a == 0 ? prev_pre : (sk[a - 1] >> pre_sh);
-            if ((sk[a] >> pre_sh) != pr) {
-                flags |= 1u << q;
-                ++cntf;
-            }
-        }
-    }
-    uint32_t x = cntf;
+    uint32_t x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
@@ -246,464 +72,966 @@ __global__ void __launch_bounds__(256) segsort_window(uint64_t* __restrict__ key
     }
     if (lane == 31) ws[warp] = x;
     __syncthreads();
-    uint32_t sid = 0;
-    for (int w = 0; w < warp; ++w) sid += ws[w];
-    sid += x - cntf;  // heads before my first position
-    if (threadIdx.x == 255) nseg_s = (int)(sid + cntf);
+    if (warp == 0) {
+        uint32_t w = lane < NT / 32 ? ws[lane] : 0u;
 #pragma unroll
-    for (int q = 0; q < PER; ++q) {
-        const int a = a0 + q;
-        if (a < len) {
-            if (flags >> q & 1u) {
-                seg_start[sid] = (uint16_t)a;
-                ++sid;
-            }
-            seg_of[a] = (uint16_t)(sid == 0 ? 0xffffu : sid - 1);  // 0xffff: previous window's segment
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
         }
+        if (lane < NT / 32) ws[lane] = w;
     }
     __syncthreads();
-    const int nseg = nseg_s;
-    for (int li = threadIdx.x; li < len; li += blockDim.x) {
-        const uint32_t sg = seg_of[li];
-        if (sg == 0xffffu) continue;
-        const int h = seg_start[sg];
-        if (h >= own) continue;                              // head in the next window
-        const int e = (int)sg + 1 < nseg ? seg_start[sg + 1] : len;
-        const uint64_t pre = sk[li] >> pre_sh;
-        const bool beyond = (e == len) && (w0 + len < n) && (k[w0 + len] >> pre_sh) == pre;
-        if (beyond || e - h > kSegCap) {
-            if (li == h) {                                   // the head reports the long segment once
-                // end of the prefix run: keys are sorted by prefix, so binary search
-                int64_t a = w0 + e, b = n;
-                while (a < b) {
-                    const int64_t mid = (a + b) >> 1;
-                    if ((k[mid] >> pre_sh) == pre) a = mid + 1;
-                    else b = mid;
-                }
-                const int64_t ge = a;
-                const uint32_t slot = atomicAdd(overflow, 1u);
-                if ((int)slot < cap) {
-                    overflow[1 + 3 * slot] = (uint32_t)t;
-                    overflow[2 + 3 * slot] = (uint32_t)(w0 + h);
-                    overflow[3 + 3 * slot] = (uint32_t)ge;
-                }
-            }
-            continue;
+    const uint32_t r = (warp ? ws[warp - 1] : 0u) + x - v;
+    if (total) *total = ws[NT / 32 - 1];
+    __syncthreads();
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// L1 digit selection: the top B1 key bits that VARY over the table.  SRP keys
+// have constant bits (sketch bins with no coordinate, sign patterns shared by a
+// cluster), so a fixed top-bits digit would collapse into a few huge bins.
+// Extracting varying bits keeps key order (the other bits are constant).
+// ---------------------------------------------------------------------------
+struct L1Spec {
+    uint64_t below;   // key bits below the lowest digit bit: what the per-bin sort still orders
+    int32_t nbits;    // digit bits (<= B1; fewer when fewer key bits vary)
+    int32_t shift;    // contiguous digit: (key >> shift) & (2^nbits - 1); -1: gather pos[]
+    uint8_t pos[12];  // digit bit positions, most significant first
+};
+
+__device__ __forceinline__ uint32_t l1_digit(uint64_t k, const L1Spec& s) {
+    if (s.shift >= 0) return (uint32_t)(k >> s.shift) & ((1u << s.nbits) - 1u);
+    uint32_t d = 0;
+#pragma unroll
+    for (int j = 0; j < 11; ++j)
+        if (j < s.nbits) d = (d << 1) | (uint32_t)((k >> s.pos[j]) & 1ull);
+    return d;
+}
+
+// OR of the keys and OR of their complements per table (varying bits = both set).
+__global__ void __launch_bounds__(256) g0_mask(const uint64_t* __restrict__ keys, int64_t n,
+                                               unsigned long long* __restrict__ vm) {
+    const int t = blockIdx.y;
+    const uint64_t* kt = keys + (int64_t)t * n;
+    uint64_t o = 0, no = 0;
+    const int64_t i0 = (int64_t)blockIdx.x * 8192 + threadIdx.x;
+#pragma unroll 8
+    for (int r = 0; r < 32; ++r) {
+        const int64_t i = i0 + r * 256;
+        if (i < n) {
+            const uint64_t k = __ldcs(kt + i);
+            o |= k;
+            no |= ~k;
         }
-        if (e - h == 1) continue;
-        const uint64_t kv = sk[li];
-        int rank = 0;
-        for (int j = h; j < e; ++j) {
-            const uint64_t kj = sk[j];
-            rank += (kj < kv || (kj == kv && j < li)) ? 1 : 0;
-        }
-        k[w0 + h + rank] = kv;
-        d[w0 + h + rank] = si[li];
+    }
+#pragma unroll
+    for (int sft = 16; sft > 0; sft >>= 1) {
+        o |= __shfl_xor_sync(0xffffffffu, o, sft);
+        no |= __shfl_xor_sync(0xffffffffu, no, sft);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicOr(vm + 2 * t, (unsigned long long)o);
+        atomicOr(vm + 2 * t + 1, (unsigned long long)no);
     }
 }
 
-// Sorting network with ascending comparators only (bitonic sort with a "flip" first
-// merge step), so indices >= len behave as +infinity and need no padding.
-template <typename KeyAt, typename Swap>
-__device__ void ascending_network(int64_t len, KeyAt less_at, Swap swap_at, bool smem) {
-    int64_t P = 1;
-    while (P < len) P <<= 1;
-    for (int64_t size = 2; size <= P; size <<= 1) {
-        for (int64_t stride = size >> 1; stride > 0; stride >>= 1) {
-            const bool flip = (stride == (size >> 1));
-            for (int64_t i = threadIdx.x; i < (P >> 1); i += blockDim.x) {
-                int64_t a, b;
-                if (flip) {
-                    const int64_t blk = i / stride, j = i % stride;
-                    a = blk * size + j;
-                    b = blk * size + size - 1 - j;
-                } else {
-                    a = (i / stride) * 2 * stride + (i % stride);
-                    b = a + stride;
-                }
-                if (b < len && less_at(b, a)) swap_at(a, b);
-            }
-            if (smem) __syncthreads();
-            else {
-                __threadfence_block();
-                __syncthreads();
-            }
-        }
+__device__ L1Spec make_spec(const int* pos, int nb) {
+    L1Spec s;
+    s.nbits = nb;
+    for (int j = 0; j < 12; ++j) s.pos[j] = j < nb ? (uint8_t)pos[j] : 0;
+    if (nb == 0) {
+        s.shift = 0;
+        s.below = ~0ull;
+    } else {
+        const int lo = pos[nb - 1];
+        s.shift = (pos[0] - lo == nb - 1) ? lo : -1;
+        s.below = (1ull << lo) - 1ull;
     }
+    return s;
 }
 
-// Long equal-prefix segment (many equal keys, e.g. duplicate points or empty codes):
-// one CTA runs a stable LSD radix sort of the segment on the key bits below the
-// common prefix (8-bit digits, digits that are constant over the segment are
-// skipped), ping-ponging with the free scratch buffers.  Items arrive id-ascending
-// and every pass is stable, so the result is the (key, id) order.
-__device__ void cta_radix_segment(uint64_t* k, uint32_t* d, uint64_t* k2, uint32_t* d2, int64_t len, int low_bits,
-                                  uint32_t* s_cnt, uint32_t* s_wcnt, uint32_t* s_woff, uint64_t* s_red) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    // which digits vary across the segment?
-    uint64_t orv = 0, andv = ~0ull;
-    for (int64_t a = threadIdx.x; a < len; a += blockDim.x) {
-        orv |= k[a];
-        andv &= k[a];
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        orv |= __shfl_xor_sync(0xffffffffu, orv, o);
-        andv &= __shfl_xor_sync(0xffffffffu, andv, o);
-    }
-    if (lane == 0) {
-        s_red[2 * warp] = orv;
-        s_red[2 * warp + 1] = andv;
-    }
-    __syncthreads();
-    orv = 0;
-    andv = ~0ull;
-    for (int w = 0; w < nw; ++w) {
-        orv |= s_red[2 * w];
-        andv &= s_red[2 * w + 1];
-    }
-    const uint64_t varying = orv ^ andv;
-    __syncthreads();
-    uint64_t *src_k = k, *dst_k = k2;
-    uint32_t *src_d = d, *dst_d = d2;
-    for (int sh = 0; sh < low_bits; sh += 8) {
-        if (((varying >> sh) & 255u) == 0) continue;
-        // histogram
-        for (int i = threadIdx.x; i < 256; i += blockDim.x) s_cnt[i] = 0;
-        __syncthreads();
-        for (int64_t a = threadIdx.x; a < len; a += blockDim.x) atomicAdd(&s_cnt[(src_k[a] >> sh) & 255u], 1u);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t acc = 0;
-            for (int i = 0; i < 256; ++i) {
-                const uint32_t c = s_cnt[i];
-                s_cnt[i] = acc;
-                acc += c;
-            }
-        }
-        __syncthreads();
-        // stable scatter in rounds of blockDim items
-        for (int64_t base = 0; base < len; base += blockDim.x) {
-            const int64_t a = base + threadIdx.x;
-            const bool valid = a < len;
-            const uint64_t key = valid ? src_k[a] : 0;
-            const uint32_t id = valid ? src_d[a] : 0;
-            const uint32_t dg = valid ? (uint32_t)(key >> sh) & 255u : 256u;
-            const uint32_t peers = __match_any_sync(0xffffffffu, dg);
-            const uint32_t rank = __popc(peers & lanemask_lt());
-            for (int i = threadIdx.x; i < nw * 256; i += blockDim.x) s_wcnt[i] = 0;
-            __syncthreads();
-            if (valid && rank == 0) s_wcnt[warp * 256 + dg] = __popc(peers);
-            __syncthreads();
-            for (int dd = threadIdx.x; dd < 256; dd += blockDim.x) {
-                uint32_t acc = s_cnt[dd];
-                for (int w = 0; w < nw; ++w) {
-                    s_woff[w * 256 + dd] = acc;
-                    acc += s_wcnt[w * 256 + dd];
-                }
-                s_cnt[dd] = acc;
-            }
-            __syncthreads();
-            if (valid) {
-                const uint32_t pos = s_woff[warp * 256 + dg] + rank;
-                dst_k[pos] = key;
-                dst_d[pos] = id;
-            }
-            __syncthreads();
-        }
-        uint64_t* tk = src_k;
-        src_k = dst_k;
-        dst_k = tk;
-        uint32_t* td = src_d;
-        src_d = dst_d;
-        dst_d = td;
-        __threadfence_block();
-        __syncthreads();
-    }
-    if (src_k != k) {  // odd number of passes: copy back
-        for (int64_t a = threadIdx.x; a < len; a += blockDim.x) {
-            k[a] = src_k[a];
-            d[a] = src_d[a];
-        }
-    }
-}
-
-__global__ void __launch_bounds__(1024) segsort_big(uint64_t* __restrict__ keys, uint32_t* __restrict__ ids,
-                                                    uint64_t* __restrict__ scratch_k, uint32_t* __restrict__ scratch_d,
-                                                    int64_t n, int low_bits, const uint32_t* overflow, int cap,
-                                                    int* flags) {
-    extern __shared__ __align__(16) unsigned char sm[];
-    uint64_t* sk = reinterpret_cast<uint64_t*>(sm);
-    uint32_t* si = reinterpret_cast<uint32_t*>(sm + kSegBig * sizeof(uint64_t));
-    __shared__ uint32_t s_cnt[256];
-    __shared__ uint64_t s_red[64];
-    const uint32_t count = min(overflow[0], (uint32_t)cap);
-    if (blockIdx.x == 0 && threadIdx.x == 0 && overflow[0] > (uint32_t)cap) atomicOr(flags, 4);
-    for (uint32_t e = blockIdx.x; e < count; e += gridDim.x) {
-        const int t = overflow[1 + 3 * e];
-        const int64_t lo = overflow[2 + 3 * e], hi = overflow[3 + 3 * e];
-        uint64_t* k = keys + (int64_t)t * n + lo;
-        uint32_t* d = ids + (int64_t)t * n + lo;
-        const int64_t len = hi - lo;
-        {   // all keys equal (repeated code tuples): already in id order
-            __shared__ int s_neq;
-            if (threadIdx.x == 0) s_neq = 0;
-            __syncthreads();
-            const uint64_t k0 = k[0];
-            int neq = 0;
-            for (int64_t a = threadIdx.x; a < len && !neq; a += blockDim.x) neq = k[a] != k0;
-            if (neq) s_neq = 1;
-            __syncthreads();
-            const int any = s_neq;
-            __syncthreads();
-            if (!any) continue;
-        }
-        // the per-warp count tables live in the dynamic smem area (unused by the partition)
-        uint32_t* s_wcnt = reinterpret_cast<uint32_t*>(sm);
-        uint32_t* s_woff = s_wcnt + 32 * 256;
-        uint64_t* k2 = scratch_k + (int64_t)t * n + lo;
-        uint32_t* d2 = scratch_d + (int64_t)t * n + lo;
-        // Long segments are dominated by repeated keys (duplicate points, empty codes):
-        // stable 3-way partition around the middle item's key first; the "equal" part is
-        // already in id order, only the rest needs sorting.
-        const uint64_t pivot = k[len / 2];
-        __shared__ uint32_t s_lt, s_eq;
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-        if (threadIdx.x == 0) {
-            s_lt = 0;
-            s_eq = 0;
-        }
-        __syncthreads();
-        {
-            uint32_t lt = 0, eq = 0;
-            for (int64_t a = threadIdx.x; a < len; a += blockDim.x) {
-                lt += k[a] < pivot;
-                eq += k[a] == pivot;
-            }
-            atomicAdd(&s_lt, lt);
-            atomicAdd(&s_eq, eq);
-        }
-        __syncthreads();
-        const uint32_t nlt = s_lt, neq = s_eq;
-        uint32_t base0 = 0, base1 = nlt, base2 = nlt + neq;
-        for (int64_t b0 = 0; b0 < len; b0 += blockDim.x) {
-            const int64_t a = b0 + threadIdx.x;
-            const bool valid = a < len;
-            const uint64_t key = valid ? k[a] : 0;
-            const uint32_t cls = !valid ? 3u : (key < pivot ? 0u : (key == pivot ? 1u : 2u));
-            const uint32_t m0 = __ballot_sync(0xffffffffu, cls == 0), m1 = __ballot_sync(0xffffffffu, cls == 1),
-                           m2 = __ballot_sync(0xffffffffu, cls == 2);
-            if (lane == 0) {
-                s_wcnt[warp * 3 + 0] = __popc(m0);
-                s_wcnt[warp * 3 + 1] = __popc(m1);
-                s_wcnt[warp * 3 + 2] = __popc(m2);
-            }
-            __syncthreads();
-            uint32_t pre0 = base0, pre1 = base1, pre2 = base2;
-            for (int w = 0; w < warp; ++w) {
-                pre0 += s_wcnt[w * 3];
-                pre1 += s_wcnt[w * 3 + 1];
-                pre2 += s_wcnt[w * 3 + 2];
-            }
-            const uint32_t lm = (1u << lane) - 1u;
-            if (valid) {
-                const uint32_t pos = cls == 0 ? pre0 + __popc(m0 & lm) : cls == 1 ? pre1 + __popc(m1 & lm)
-                                                                                  : pre2 + __popc(m2 & lm);
-                k2[pos] = key;
-                d2[pos] = d[a];
-            }
-            for (int w = 0; w < nw; ++w) {
-                base0 += s_wcnt[w * 3];
-                base1 += s_wcnt[w * 3 + 1];
-                base2 += s_wcnt[w * 3 + 2];
-            }
-            __syncthreads();
-        }
-        __threadfence_block();
-        __syncthreads();
-        for (int64_t a = threadIdx.x; a < len; a += blockDim.x) {
-            k[a] = k2[a];
-            d[a] = d2[a];
-        }
-        __threadfence_block();
-        __syncthreads();
-        const int64_t ngt = len - nlt - neq;
-        const int64_t part_lo[2] = {0, (int64_t)nlt + neq};
-        const int64_t part_len[2] = {(int64_t)nlt, ngt};
-        for (int q = 0; q < 2; ++q) {
-            const int64_t plen = part_len[q];
-            if (plen <= 1) continue;
-            uint64_t* pk = k + part_lo[q];
-            uint32_t* pd = d + part_lo[q];
-            if (plen <= kSegBig) {
-                for (int64_t a = threadIdx.x; a < plen; a += blockDim.x) {
-                    sk[a] = pk[a];
-                    si[a] = pd[a];
-                }
-                __syncthreads();
-                ascending_network(
-                    plen, [&](int64_t x, int64_t y) { return kless(sk[x], si[x], sk[y], si[y]); },
-                    [&](int64_t x, int64_t y) {
-                        const uint64_t tk = sk[x]; sk[x] = sk[y]; sk[y] = tk;
-                        const uint32_t ti = si[x]; si[x] = si[y]; si[y] = ti;
-                    },
-                    true);
-                for (int64_t a = threadIdx.x; a < plen; a += blockDim.x) {
-                    pk[a] = sk[a];
-                    pd[a] = si[a];
-                }
-                __syncthreads();
-            } else {
-                cta_radix_segment(pk, pd, k2 + part_lo[q], d2 + part_lo[q], plen, low_bits, s_cnt, s_wcnt, s_woff,
-                                  s_red);
-            }
-        }
-        __syncthreads();
-    }
-}
-
-__global__ void __launch_bounds__(kRT) rle_count(const uint64_t* __restrict__ keys, int64_t n, uint32_t* tile_aux,
-                                                 int T) {
-    __shared__ uint32_t c;
-    const int t = blockIdx.y, tile = blockIdx.x;
-    if (threadIdx.x == 0) c = 0;
-    __syncthreads();
-    const uint64_t* k = keys + (int64_t)t * n;
-    uint32_t local = 0;
-    for (int r = 0; r < kRounds; ++r) {
-        const int64_t i = (int64_t)tile * kTile + r * kRT + threadIdx.x;
-        if (i < n && (i == 0 || k[i] != k[i - 1])) ++local;
-    }
-    atomicAdd(&c, local);
-    __syncthreads();
-    if (threadIdx.x == 0) tile_aux[(int64_t)t * (T + 1) + tile] = c;
-}
-
-__global__ void __launch_bounds__(kRT) rle_write(const uint64_t* __restrict__ keys, int64_t n,
-                                                 const uint32_t* tile_aux, int T, IndexDev out) {
-    __shared__ uint32_t wsum[kRT / 32];
-    __shared__ uint32_t base_s;
-    const int t = blockIdx.y, tile = blockIdx.x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t* k = keys + (int64_t)t * n;
-    if (threadIdx.x == 0) base_s = tile_aux[(int64_t)t * (T + 1) + tile];
-    __syncthreads();
-    for (int r = 0; r < kRounds; ++r) {
-        const int64_t i = (int64_t)tile * kTile + r * kRT + threadIdx.x;
-        const bool head = i < n && (i == 0 || k[i] != k[i - 1]);
-        const uint32_t ball = __ballot_sync(0xffffffffu, head);
-        if (lane == 0) wsum[warp] = __popc(ball);
-        __syncthreads();
-        uint32_t before = base_s;
-        for (int w = 0; w < warp; ++w) before += wsum[w];
-        if (head) {
-            const uint32_t b = before + __popc(ball & lanemask_lt());
-            out.ukeys[(int64_t)t * n + b] = k[i];
-            out.offs[(int64_t)t * (n + 1) + b] = (uint32_t)i;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t s = 0;
-            for (int w = 0; w < kRT / 32; ++w) s += wsum[w];
-            base_s += s;
-        }
-        __syncthreads();
-    }
-}
-
-__global__ void rle_finish(IndexDev out, const uint32_t* tile_aux, int T, int64_t n, int L) {
+// passes == 1 (MSD): the top B1 varying bits.  passes == 2 (LSD, narrow keys): the
+// varying bits split into a low half (pass 0) and a high half (pass 1), each <= B1.
+__global__ void g0_spec(const unsigned long long* __restrict__ vm, int L, int B1, int passes,
+                        L1Spec* __restrict__ spec) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= L) return;
-    const uint32_t nb = tile_aux[(int64_t)t * (T + 1) + T];
-    out.nb[t] = nb;
-    out.offs[(int64_t)t * (n + 1) + nb] = (uint32_t)n;
+    const uint64_t V = vm[2 * t] & vm[2 * t + 1];
+    int pos[64];
+    int v = 0;
+    for (int b = 63; b >= 0; --b)
+        if ((V >> b) & 1ull) pos[v++] = b;
+    if (passes == 1) {
+        spec[t] = make_spec(pos, v < B1 ? v : B1);
+    } else {
+        const int hi_n = min(B1, (v + 1) / 2);
+        const int lo_n = min(B1, v - hi_n);
+        spec[(int64_t)L + t] = make_spec(pos, hi_n);   // pass 1: most significant half
+        spec[t] = make_spec(pos + hi_n, lo_n);          // pass 0
+    }
+}
+
+// ---------------------------------------------------------------------------
+// L1: histogram, per-bin tile scan, bin starts, stable scatter
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kG1Threads) g1_hist(const uint64_t* __restrict__ keys, int64_t n,
+                                                    const L1Spec* __restrict__ spec, int nb1,
+                                                    uint32_t* __restrict__ hist, int T) {
+    extern __shared__ uint32_t g1_cnt[];
+    const int t = blockIdx.y, tile = blockIdx.x;
+    for (int i = threadIdx.x; i < nb1; i += kG1Threads) g1_cnt[i] = 0;
+    const int64_t t0 = (int64_t)tile * kG1Tile;
+    const uint64_t* kt = keys + (int64_t)t * n + t0;
+    const int cn = (int)min((int64_t)kG1Tile, n - t0);
+    const L1Spec sp = spec[t];
+    uint64_t k[kG1Tile / kG1Threads];
+#pragma unroll
+    for (int r = 0; r < kG1Tile / kG1Threads; ++r) {
+        const int i = r * kG1Threads + threadIdx.x;
+        k[r] = i < cn ? __ldcs(kt + i) : 0ull;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kG1Tile / kG1Threads; ++r) {
+        const int i = r * kG1Threads + threadIdx.x;
+        if (i < cn) atomicAdd(&g1_cnt[l1_digit(k[r], sp)], 1u);
+    }
+    __syncthreads();
+    uint32_t* row = hist + ((int64_t)t * T + tile) * nb1;
+    for (int b = threadIdx.x; b < nb1; b += kG1Threads) row[b] = g1_cnt[b];
+}
+
+// One warp per (table, 32 consecutive bins), lane = bin: exclusive running sum over
+// the tiles in place (coalesced rows of the tile-major counts), bin totals out.
+__global__ void g1_scan(uint32_t* __restrict__ hist, int T, int L, int nb1, uint32_t* __restrict__ tot) {
+    const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int groups = (nb1 + 31) / 32;
+    if (wg >= (int64_t)L * groups) return;
+    const int t = (int)(wg / groups), b = (int)(wg % groups) * 32 + lane;
+    if (b >= nb1) return;
+    uint32_t* col = hist + (int64_t)t * T * nb1 + b;
+    uint32_t run = 0;
+    int tile = 0;
+    for (; tile + 4 <= T; tile += 4) {
+        const uint32_t v0 = col[(int64_t)tile * nb1], v1 = col[(int64_t)(tile + 1) * nb1],
+                       v2 = col[(int64_t)(tile + 2) * nb1], v3 = col[(int64_t)(tile + 3) * nb1];
+        col[(int64_t)tile * nb1] = run;
+        col[(int64_t)(tile + 1) * nb1] = run + v0;
+        col[(int64_t)(tile + 2) * nb1] = run + v0 + v1;
+        col[(int64_t)(tile + 3) * nb1] = run + v0 + v1 + v2;
+        run += v0 + v1 + v2 + v3;
+    }
+    for (; tile < T; ++tile) {
+        const uint32_t v = col[(int64_t)tile * nb1];
+        col[(int64_t)tile * nb1] = run;
+        run += v;
+    }
+    tot[(int64_t)t * nb1 + b] = run;
+}
+
+// One block per table: bin starts = exclusive scan of the bin totals, and (MSD
+// path) the L2 chunk edges: chunkbin[c] = first bin whose start is >= c*span.
+__global__ void __launch_bounds__(1024) g1_binstart(const uint32_t* __restrict__ tot, int nb1, int64_t n,
+                                                    uint32_t* __restrict__ binstart, int span, int nchunks,
+                                                    uint32_t* __restrict__ chunkbin) {
+    __shared__ uint32_t ws[32];
+    __shared__ uint32_t sbs[2049];
+    const int t = blockIdx.x;
+    const int b0 = 2 * threadIdx.x, b1 = b0 + 1;
+    const uint32_t v0 = b0 < nb1 ? tot[(int64_t)t * nb1 + b0] : 0u;
+    const uint32_t v1 = b1 < nb1 ? tot[(int64_t)t * nb1 + b1] : 0u;
+    const uint32_t e = block_excl_scan<1024>(v0 + v1, ws, nullptr);
+    uint32_t* bs = binstart + (int64_t)t * (nb1 + 1);
+    if (b0 < nb1) sbs[b0] = bs[b0] = e;
+    if (b1 < nb1) sbs[b1] = bs[b1] = e + v0;
+    if (threadIdx.x == 0) sbs[nb1] = bs[nb1] = (uint32_t)n;
+    if (!chunkbin) return;
+    __syncthreads();
+    uint32_t* cb = chunkbin + (int64_t)t * (nchunks + 1);
+    for (int b = threadIdx.x; b <= nb1; b += blockDim.x) {
+        // chunks c with bs[b-1] < c*span <= bs[b] start at bin b (b == nb1: past the end)
+        const int64_t prev = b ? (int64_t)sbs[b - 1] : -1;
+        const int64_t cur = sbs[b];
+        const int64_t c0 = prev < 0 ? 0 : prev / span + 1;
+        const int64_t c1 = min((int64_t)nchunks - 1, cur / span);
+        for (int64_t c = c0; c <= c1; ++c) cb[c] = (uint32_t)b;
+    }
+    if (threadIdx.x == 0) cb[nchunks] = (uint32_t)nb1;
+}
+
+// Stable scatter of one 4096-item tile by its L1 digit.  Warp w owns items
+// [512w, 512w+512) of the tile (coalesced 32-item rounds) and ranks them with
+// match_any against warp-private running digit counts; one block pass turns
+// (digit, warp) counts into offsets; items are staged in digit order in shared
+// memory and written so that consecutive threads write consecutive addresses.
+template <bool IMPLICIT_IDS>
+__global__ void __launch_bounds__(kG1Threads, 3)
+    g1_scatter(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ iin, uint64_t* __restrict__ kout,
+               uint32_t* __restrict__ iout, int64_t n, const L1Spec* __restrict__ spec, int nb1,
+               const uint32_t* __restrict__ hist,
+               const uint32_t* __restrict__ binstart, int T, uint32_t id_base) {
+    extern __shared__ __align__(16) unsigned char g1_dsm[];
+    uint64_t* sk = reinterpret_cast<uint64_t*>(g1_dsm);                 // [kG1Tile]
+    uint32_t* si = reinterpret_cast<uint32_t*>(g1_dsm + kG1Tile * 8);   // [kG1Tile]
+    uint32_t* gpos = reinterpret_cast<uint32_t*>(g1_dsm + kG1Tile * 12);  // [nb1] global start of the tile's run
+    uint32_t* loc = gpos + nb1;                                         // [nb1] staged start of the digit
+    uint16_t* sd = reinterpret_cast<uint16_t*>(loc + nb1);              // [kG1Tile] staged digit
+    uint16_t* wrun = sd + kG1Tile;                                      // [kG1Warps][nb1]
+    __shared__ uint32_t ws[32];
+    const int t = blockIdx.y, tile = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const L1Spec sp = spec[t];
+    for (int i = threadIdx.x; i < kG1Warps * nb1; i += kG1Threads) wrun[i] = 0;
+    const int64_t tb = (int64_t)t * n;
+    const int64_t base = (int64_t)tile * kG1Tile + warp * kG1PerWarp;
+    uint64_t key[kG1Rounds];
+    uint32_t slot[kG1Rounds];
+#pragma unroll
+    for (int r = 0; r < kG1Rounds; ++r) {
+        const int64_t i = base + r * 32 + lane;
+        key[r] = i < n ? __ldcs(kin + tb + i) : 0ull;
+    }
+    __syncthreads();
+    uint16_t* my = wrun + warp * nb1;
+    // all digit matches first (independent, pipelined), then the ordered running counts
+    uint32_t peers[kG1Rounds];
+#pragma unroll
+    for (int r = 0; r < kG1Rounds; ++r) {
+        const int64_t i = base + r * 32 + lane;
+        slot[r] = i < n ? l1_digit(key[r], sp) : 0x10000u + lane;
+        peers[r] = __match_any_sync(0xffffffffu, slot[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < kG1Rounds; ++r) {
+        const uint32_t dg = slot[r];
+        const bool valid = dg < 0x10000u;
+        const uint32_t rank = __popc(peers[r] & lanemask_lt());
+        const uint32_t before = valid ? my[dg] : 0u;
+        __syncwarp();
+        if (valid && rank == 0) my[dg] = (uint16_t)(before + __popc(peers[r]));
+        __syncwarp();
+        slot[r] = (dg << 16) | (before + rank);
+    }
+    __syncthreads();
+    // per digit: exclusive over warps (in place), tile count; exclusive over digits -> loc
+    const int DPT = (nb1 + kG1Threads - 1) / kG1Threads;
+    uint32_t mysum = 0;
+    for (int j = 0; j < DPT; ++j) {
+        const int d = threadIdx.x * DPT + j;
+        if (d < nb1) {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int w = 0; w < kG1Warps; ++w) {
+                const uint32_t c = wrun[w * nb1 + d];
+                wrun[w * nb1 + d] = (uint16_t)acc;
+                acc += c;
+            }
+            loc[d] = acc;
+            mysum += acc;
+        }
+    }
+    uint32_t ex = block_excl_scan<kG1Threads>(mysum, ws, nullptr);
+    for (int j = 0; j < DPT; ++j) {
+        const int d = threadIdx.x * DPT + j;
+        if (d < nb1) {
+            const uint32_t c = loc[d];
+            loc[d] = ex;
+            ex += c;
+            gpos[d] = binstart[(int64_t)t * (nb1 + 1) + d] + hist[((int64_t)t * T + tile) * nb1 + d];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kG1Rounds; ++r) {
+        const int64_t i = base + r * 32 + lane;
+        if (i < n) {
+            const uint32_t dg = slot[r] >> 16;
+            const uint32_t p = loc[dg] + wrun[warp * nb1 + dg] + (slot[r] & 0xffffu);
+            sk[p] = key[r];
+            sd[p] = (uint16_t)dg;
+            si[p] = IMPLICIT_IDS ? id_base + (uint32_t)i : iin[tb + i];
+        }
+    }
+    __syncthreads();
+    const int cnt = (int)min((int64_t)kG1Tile, n - (int64_t)tile * kG1Tile);
+    for (int p = threadIdx.x; p < cnt; p += kG1Threads) {
+        const uint64_t k = sk[p];
+        const uint32_t dg = sd[p];
+        const uint32_t pos = gpos[dg] + ((uint32_t)p - loc[dg]);
+        kout[tb + pos] = k;
+        iout[tb + pos] = si[p];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// L2: per-bin sort + run-length encoding + chained bucket numbering
+// ---------------------------------------------------------------------------
+struct G2Args {
+    const uint64_t* keys;       // L1 output [L][n]
+    const uint32_t* ids;        // L1 output [L][n]
+    const uint32_t* binstart;   // [L][nb1+1]
+    unsigned long long* state;  // [L][nb1] look-back words: (flag << 32) | count
+    uint32_t* scratch;          // [L][2n] permutation ping-pong of bins too large for shared memory
+    const L1Spec* spec;         // [L]
+    int64_t n;
+    int nb1;
+    int nchunks;                // L2 chunks per table
+    const uint32_t* chunkbin;   // [L][nchunks+1] first L1 bin of every chunk
+    IndexDev out;
+};
+
+template <typename PT>
+__device__ __forceinline__ uint32_t pget(const PT* p, int64_t r) {
+    return p ? (uint32_t)p[r] : (uint32_t)r;
+}
+
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Decoupled look-back over the bins of one table, one warp: publishes this bin's
+// bucket count and returns the number of buckets in all earlier bins.  The warp
+// inspects 32 predecessors per step (lane 0 = nearest) and stops at the nearest
+// inclusive prefix.  Bins of a table are launched in increasing block order, so
+// predecessors are running.
+__device__ uint32_t chained_prefix_warp(unsigned long long* st, int b, uint32_t agg) {
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) st_release(st + b, ((b == 0 ? 2ull : 1ull) << 32) | agg);
+    if (b == 0) return 0;
+    uint32_t acc = 0;
+    int j = b - 1;
+    while (true) {
+        const int idx = j - lane;
+        const unsigned long long v = idx >= 0 ? ld_acquire(st + idx) : (2ull << 32);
+        const uint32_t f = (uint32_t)(v >> 32);
+        const uint32_t incl = __ballot_sync(0xffffffffu, f == 2);
+        const uint32_t notready = __ballot_sync(0xffffffffu, f == 0);
+        const int first = incl ? __ffs(incl) - 1 : 31;
+        const uint32_t need = (first == 31) ? 0xffffffffu : ((2u << first) - 1u);
+        if (notready & need) {
+            __nanosleep(64);
+            continue;
+        }
+        uint32_t val = (lane <= first) ? (uint32_t)v : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+        acc += val;
+        if (incl) break;
+        j -= 32;
+    }
+    if (lane == 0) st_release(st + b, (2ull << 32) | (acc + agg));
+    return acc;
+}
+
+// Bits that vary over K[0..len) (OR ^ AND).
+__device__ uint64_t cta_varying(const uint64_t* K, int64_t len, unsigned long long* red) {
+    if (threadIdx.x == 0) {
+        red[0] = 0ull;
+        red[1] = ~0ull;
+    }
+    __syncthreads();
+    uint64_t o = 0, a = ~0ull;
+    for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
+        const uint64_t k = K[i];
+        o |= k;
+        a &= k;
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        o |= __shfl_xor_sync(0xffffffffu, o, s);
+        a &= __shfl_xor_sync(0xffffffffu, a, s);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicOr(&red[0], (unsigned long long)o);
+        atomicAnd(&red[1], (unsigned long long)a);
+    }
+    __syncthreads();
+    const uint64_t v = len > 0 ? (red[0] ^ red[1]) : 0ull;
+    __syncthreads();
+    return v;
+}
+
+// Stable counting pass on the 8-bit digit at `sh` of K[src[i]], i < len; dst
+// receives src in digit order (src == nullptr: identity).  Warps own contiguous
+// ranges; per-warp digit counts -> (digit, warp) offsets -> ranked scatter.
+struct ShiftDigit {
+    int sh;
+    __device__ __forceinline__ uint32_t operator()(uint64_t k) const { return (uint32_t)(k >> sh) & 255u; }
+};
+// (L1 bin inside the chunk, the next `w` key bits below the L1 digit at shift `sh`)
+struct ChunkDigit {
+    L1Spec sp;
+    uint32_t bin0;
+    int w, sh;
+    __device__ __forceinline__ uint32_t operator()(uint64_t k) const {
+        return ((l1_digit(k, sp) - bin0) << w) | ((uint32_t)(k >> sh) & ((1u << w) - 1u));
+    }
+};
+
+template <typename PT, typename CT, typename DF = ShiftDigit>
+__device__ void cta_digit_pass(const uint64_t* K, const PT* src, PT* dst, int64_t len, DF df, CT* wcnt,
+                               uint32_t* ws) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t per = ((len + kG2Warps - 1) / kG2Warps + 31) / 32 * 32;
+    const int64_t a0 = min(len, (int64_t)warp * per), a1 = min(len, a0 + per);
+    for (int i = threadIdx.x; i < kG2Warps * 256; i += kG2Threads) wcnt[i] = 0;
+    __syncthreads();
+    CT* my = wcnt + warp * 256;
+    for (int64_t b = a0; b < a1; b += 32) {
+        const int64_t i = b + lane;
+        const bool valid = i < a1;
+        const uint32_t s = valid ? pget(src, i) : 0u;
+        const uint32_t dg = valid ? df(K[s]) : 256u + lane;
+        const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+        if (valid && (peers & lanemask_lt()) == 0) my[dg] = (CT)(my[dg] + __popc(peers));
+        __syncwarp();
+    }
+    __syncthreads();
+    {
+        const int d = threadIdx.x;
+        uint32_t tot = 0;
+        if (d < 256)
+            for (int w = 0; w < kG2Warps; ++w) tot += wcnt[w * 256 + d];
+        uint32_t acc = block_excl_scan<kG2Threads>(tot, ws, nullptr);
+        if (d < 256)
+            for (int w = 0; w < kG2Warps; ++w) {
+                const uint32_t c = wcnt[w * 256 + d];
+                wcnt[w * 256 + d] = (CT)acc;
+                acc += c;
+            }
+    }
+    __syncthreads();
+    for (int64_t b = a0; b < a1; b += 32) {
+        const int64_t i = b + lane;
+        const bool valid = i < a1;
+        const uint32_t s = valid ? pget(src, i) : 0u;
+        const uint32_t dg = valid ? df(K[s]) : 256u + lane;
+        const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+        const uint32_t rank = __popc(peers & lanemask_lt());
+        const uint32_t before = valid ? (uint32_t)my[dg] : 0u;
+        __syncwarp();
+        if (valid) {
+            dst[before + rank] = (PT)s;
+            if (rank == 0) my[dg] = (CT)(before + __popc(peers));
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+}
+
+// LSD passes over the 8-bit digits below `top` that vary (bit set in `varying`);
+// the permutation starts in *cur (nullptr = identity) and ends in *cur.  Both
+// ping-pong buffers are [len].
+template <typename PT, typename CT>
+__device__ void cta_lsd(const uint64_t* K, PT*& cur, PT* b0, PT* b1, int64_t len, int top, uint64_t varying, CT* wcnt,
+                        uint32_t* ws) {
+    for (int sh = 0; sh < top; sh += 8) {
+        const uint64_t dmask = (top - sh >= 8 ? 0xffull : ((1ull << (top - sh)) - 1)) << sh;
+        if ((varying & dmask) == 0) continue;
+        PT* dst = (cur == b0) ? b1 : b0;
+        cta_digit_pass<PT, CT>(K, cur, dst, len, ShiftDigit{sh}, wcnt, ws);
+        cur = dst;
+    }
+}
+
+// Bucket count, chained numbering, and the outputs of one bin.  Each thread owns
+// a run of consecutive sorted positions: one block scan numbers the buckets.
+template <typename PT>
+__device__ void cta_emit(const uint64_t* K, const uint32_t* ID, const PT* perm, int64_t len, int64_t lo, int t,
+                         int bin, const G2Args& a, uint32_t* ws, uint32_t* bc) {
+    const int64_t vp = (len + kG2Threads - 1) / kG2Threads;
+    const int64_t r0 = min(len, (int64_t)threadIdx.x * vp), r1 = min(len, r0 + vp);
+    uint32_t u = 0;
+    {
+        uint64_t prev = r0 > 0 ? K[pget(perm, r0 - 1)] : 0ull;
+        for (int64_t r = r0; r < r1; ++r) {
+            const uint64_t k = K[pget(perm, r)];
+            u += (r == 0 || k != prev) ? 1u : 0u;
+            prev = k;
+        }
+    }
+    uint32_t utot;
+    const uint32_t ex = block_excl_scan<kG2Threads>(u, ws, &utot);
+    if (threadIdx.x < 32) {
+        const uint32_t pre = chained_prefix_warp(a.state + (int64_t)t * a.nchunks, bin, utot);
+        if (threadIdx.x == 0) *bc = pre;
+    }
+    __syncthreads();
+    const uint32_t base = *bc;
+    const int64_t n = a.n;
+    uint64_t* uk = a.out.ukeys + (int64_t)t * n;
+    uint32_t* of = a.out.offs + (int64_t)t * (n + 1);
+    uint32_t* od = a.out.ids + (int64_t)t * n + lo;
+    {
+        uint32_t ub = base + ex;
+        uint64_t prev = r0 > 0 ? K[pget(perm, r0 - 1)] : 0ull;
+        for (int64_t r = r0; r < r1; ++r) {
+            const uint64_t k = K[pget(perm, r)];
+            if (r == 0 || k != prev) {
+                uk[ub] = k;
+                of[ub] = (uint32_t)(lo + r);
+                ++ub;
+            }
+            prev = k;
+        }
+    }
+    for (int64_t r = threadIdx.x; r < len; r += kG2Threads) od[r] = ID[pget(perm, r)];
+    if (threadIdx.x == 0 && bin == a.nchunks - 1) {
+        a.out.nb[t] = base + utot;
+        of[base + utot] = (uint32_t)n;
+    }
+}
+
+// OR / AND of per-thread key aggregates over the block (red pre-initialised to {0, ~0}).
+__device__ __forceinline__ uint64_t cta_varying_from(uint64_t o, uint64_t an, unsigned long long* red) {
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        o |= __shfl_xor_sync(0xffffffffu, o, s);
+        an &= __shfl_xor_sync(0xffffffffu, an, s);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicOr(&red[0], (unsigned long long)o);
+        atomicAnd(&red[1], (unsigned long long)an);
+    }
+    __syncthreads();
+    const uint64_t v = red[0] ^ red[1];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        red[0] = 0ull;
+        red[1] = ~0ull;
+    }
+    return v;
+}
+
+__global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
+    extern __shared__ __align__(16) unsigned char g2_dsm[];
+    __shared__ uint32_t ws[32];
+    __shared__ uint32_t bc;
+    __shared__ int lst[2 * kG2Long];
+    __shared__ int nlst;
+    __shared__ unsigned long long red[2];
+    __shared__ uint32_t cls_cnt[3];
+    __shared__ uint32_t bm[kG2Cap / 32];
+    // Work unit: chunk c = the whole L1 bins whose start lies in [c*S, (c+1)*S); its
+    // items are contiguous and sorting them by the full key sorts them in place.
+    const int t = blockIdx.x, bin = blockIdx.y;   // tables interleaved: short look-back chains
+    const int64_t n = a.n;
+    const uint32_t* bs = a.binstart + (int64_t)t * (a.nb1 + 1);
+    const int bin_lo = a.chunkbin[(int64_t)t * (a.nchunks + 1) + bin];
+    const int bin_hi = a.chunkbin[(int64_t)t * (a.nchunks + 1) + bin + 1];
+    const int64_t lo = bs[bin_lo];
+    const int64_t len = (int64_t)bs[bin_hi] - lo;
+    const uint64_t* gk = a.keys + (int64_t)t * n + lo;
+    const uint32_t* gi = a.ids + (int64_t)t * n + lo;
+    const L1Spec sp = a.spec[t];
+    if (threadIdx.x == 0) {
+        red[0] = 0ull;
+        red[1] = ~0ull;
+        nlst = 0;
+    }
+
+    if (len <= kG2Cap) {
+        uint64_t* sk = reinterpret_cast<uint64_t*>(g2_dsm);                   // [cap]
+        uint32_t* si = reinterpret_cast<uint32_t*>(g2_dsm + kG2Cap * 8);      // [cap]
+        uint16_t* pa = reinterpret_cast<uint16_t*>(g2_dsm + kG2Cap * 12);     // [cap]
+        uint16_t* pb = pa + kG2Cap;                                           // [cap]
+        uint32_t* cnt = reinterpret_cast<uint32_t*>(pb + kG2Cap);             // [2048] two u16 counters per word
+        uint64_t o = 0, an = ~0ull;
+        for (int i = threadIdx.x; i < len; i += kG2Threads) {
+            const uint64_t k = gk[i];
+            sk[i] = k;
+            si[i] = gi[i];
+            o |= k;
+            an &= k;
+        }
+        __syncthreads();
+        // bits that still vary inside the L1 bins (the bins of the chunk are in order)
+        const uint64_t varying = cta_varying_from(o, an, red) & (len > 0 ? sp.below : 0ull);
+        const int hb = varying ? 64 - __clzll((long long)varying) : 0;
+        const int G = bin_hi - bin_lo;
+        const int gb = G > 1 ? 32 - __clz(G - 1) : 0;    // bits of the bin index inside the chunk
+        uint16_t* cur = nullptr;
+        if (hb == 0 && G <= 1) {
+            // one bucket (or empty): the L1 order (ids ascending) is final
+        } else if (hb + gb <= 8) {
+            // all remaining bits fit one stable 8-bit pass: (bin in chunk, bits below the digit)
+            cta_digit_pass<uint16_t, uint16_t>(sk, cur, pa, len, ChunkDigit{sp, (uint32_t)bin_lo, hb, 0},
+                                               reinterpret_cast<uint16_t*>(cnt), ws);
+            cur = pa;
+        } else {
+            // (1) counting scatter on D <= 12 bits: (bin in chunk, top Dw varying bits below
+            //     the digit); not stable, fixed in (2)
+            const int Dw = min(12 - gb, hb);
+            const int D = gb + Dw;
+            const int sh = hb - Dw;
+            const ChunkDigit cd{sp, (uint32_t)bin_lo, Dw, sh};
+            const int nw = (1 << D) > 2 ? (1 << D) >> 1 : 1;
+            for (int i = threadIdx.x; i < nw; i += kG2Threads) cnt[i] = 0u;
+            __syncthreads();
+            for (int i = threadIdx.x; i < len; i += kG2Threads) {
+                const uint32_t dg = cd(sk[i]);
+                atomicAdd(&cnt[dg >> 1], 1u << ((dg & 1u) << 4));
+            }
+            __syncthreads();
+            {
+                const int WPT = (nw + kG2Threads - 1) / kG2Threads;
+                uint32_t sm = 0;
+                for (int j = 0; j < WPT; ++j) {
+                    const int w = threadIdx.x * WPT + j;
+                    if (w < nw) {
+                        const uint32_t c = cnt[w];
+                        sm += (c & 0xffffu) + (c >> 16);
+                    }
+                }
+                uint32_t ex = block_excl_scan<kG2Threads>(sm, ws, nullptr);
+                for (int j = 0; j < WPT; ++j) {
+                    const int w = threadIdx.x * WPT + j;
+                    if (w < nw) {
+                        const uint32_t c = cnt[w], c0 = c & 0xffffu;
+                        cnt[w] = ex | ((ex + c0) << 16);
+                        ex += c0 + (c >> 16);
+                    }
+                }
+            }
+            __syncthreads();
+            for (int i = threadIdx.x; i < len; i += kG2Threads) {
+                const uint32_t dg = cd(sk[i]);
+                const uint32_t hs = (dg & 1u) << 4;
+                const uint32_t old = atomicAdd(&cnt[dg >> 1], 1u << hs);
+                pa[(old >> hs) & 0xffffu] = (uint16_t)i;
+            }
+            __syncthreads();
+            // (2) order inside segments of equal key >> sh by (key, position): O(s) ranks for
+            //     short segments; long ones by a position bitmap, then stable passes on the
+            //     bits below sh if they vary there
+            const uint16_t* src = pa;
+            uint16_t* dst = pb;
+            for (int r = threadIdx.x; r < len; r += kG2Threads) {
+                const uint32_t me = src[r];
+                const uint64_t kv = sk[me];
+                const uint64_t pr = kv >> sh;
+                const bool ep = r > 0 && (sk[src[r - 1]] >> sh) == pr;
+                const bool en = r + 1 < len && (sk[src[r + 1]] >> sh) == pr;
+                if (!ep && !en) {
+                    dst[r] = (uint16_t)me;
+                    continue;
+                }
+                int h = r;
+                while (h > 0 && r - h <= kG2Seg && (sk[src[h - 1]] >> sh) == pr) --h;
+                int e = r + 1;
+                while (e < len && e - h <= kG2Seg && (sk[src[e]] >> sh) == pr) ++e;
+                if (e - h > kG2Seg) {
+                    if (!ep) {  // head of a long segment: its end by binary search (prefixes ascend)
+                        int a0 = r + 1, b0 = (int)len;
+                        while (a0 < b0) {
+                            const int mid = (a0 + b0) >> 1;
+                            if ((sk[src[mid]] >> sh) == pr) a0 = mid + 1;
+                            else b0 = mid;
+                        }
+                        const int slot = atomicAdd(&nlst, 1);
+                        if (slot < kG2Long) {
+                            lst[2 * slot] = r;
+                            lst[2 * slot + 1] = a0;
+                        }
+                    }
+                    continue;
+                }
+                int rank = 0;
+                for (int j = h; j < e; ++j) {
+                    const uint32_t sj = src[j];
+                    const uint64_t kj = sk[sj];
+                    rank += (kj < kv || (kj == kv && sj < me)) ? 1 : 0;
+                }
+                dst[h + rank] = (uint16_t)me;
+            }
+            __syncthreads();
+            const int nl = min(nlst, kG2Long);
+            uint16_t* wc = reinterpret_cast<uint16_t*>(cnt);   // [kG2Warps][256] for the stable passes
+            for (int q = 0; q < nl; ++q) {
+                const int h = lst[2 * q], e = lst[2 * q + 1];
+                for (int w = threadIdx.x; w < kG2Cap / 32; w += kG2Threads) bm[w] = 0u;
+                __syncthreads();
+                uint64_t so = 0, sa = ~0ull;
+                for (int r = h + threadIdx.x; r < e; r += kG2Threads) {
+                    const uint32_t p = src[r];
+                    atomicOr(&bm[p >> 5], 1u << (p & 31u));
+                    const uint64_t k = sk[p];
+                    so |= k;
+                    sa &= k;
+                }
+                __syncthreads();
+                const uint32_t c = threadIdx.x < kG2Cap / 32 ? (uint32_t)__popc(bm[threadIdx.x]) : 0u;
+                uint32_t ex = block_excl_scan<kG2Threads>(c, ws, nullptr);
+                if (threadIdx.x < kG2Cap / 32) {
+                    uint32_t bits = bm[threadIdx.x];
+                    uint32_t o2 = h + ex;
+                    while (bits) {
+                        const int b = __ffs(bits) - 1;
+                        dst[o2++] = (uint16_t)(threadIdx.x * 32 + b);
+                        bits &= bits - 1u;
+                    }
+                }
+                const uint64_t v = cta_varying_from(so, sa, red) & ((sh > 0) ? ((1ull << sh) - 1ull) : 0ull);
+                if (!v) continue;  // all keys equal: position order is the final order
+                uint16_t* c2 = dst + h;
+                cta_lsd<uint16_t, uint16_t>(sk, c2, dst + h, pa + h, e - h, sh, v, wc, ws);
+                if (c2 != dst + h) {
+                    for (int r = threadIdx.x; r < e - h; r += kG2Threads) dst[h + r] = c2[r];
+                    __syncthreads();
+                }
+            }
+            cur = dst;
+        }
+        cta_emit<uint16_t>(sk, si, cur, len, lo, t, bin, a, ws, &bc);
+        return;
+    }
+
+    // ---- bin larger than shared memory: the same algorithm on global memory ----
+    uint32_t* wc = reinterpret_cast<uint32_t*>(g2_dsm);  // [kG2Warps][256] u32
+    uint32_t* p0 = a.scratch + (int64_t)t * 2 * n + lo;
+    uint32_t* p1 = p0 + n;
+    const uint64_t varying = cta_varying(gk, len, red);
+    const int sh1 = varying ? 64 - __clzll((long long)varying) : 0;
+    uint32_t* cur = nullptr;
+    if (varying) {
+        // stable 3-way split around the key at the middle position when it dominates
+        const uint64_t pivot = gk[len / 2];
+        if (threadIdx.x < 3) cls_cnt[threadIdx.x] = 0;
+        __syncthreads();
+        uint32_t lt = 0, eq = 0;
+        for (int64_t i = threadIdx.x; i < len; i += kG2Threads) {
+            const uint64_t k = gk[i];
+            lt += k < pivot;
+            eq += k == pivot;
+        }
+        atomicAdd(&cls_cnt[0], lt);
+        atomicAdd(&cls_cnt[1], eq);
+        __syncthreads();
+        const int64_t nlt = cls_cnt[0], neq = cls_cnt[1];
+        __syncthreads();
+        if (neq * 4 >= len) {
+            const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+            uint32_t base0 = 0, base1 = (uint32_t)nlt, base2 = (uint32_t)(nlt + neq);
+            for (int64_t b0 = 0; b0 < len; b0 += kG2Threads) {
+                const int64_t i = b0 + threadIdx.x;
+                const bool valid = i < len;
+                const uint64_t k = valid ? gk[i] : 0ull;
+                const uint32_t cls = !valid ? 3u : (k < pivot ? 0u : (k == pivot ? 1u : 2u));
+                const uint32_t m0 = __ballot_sync(0xffffffffu, cls == 0), m1 = __ballot_sync(0xffffffffu, cls == 1),
+                               m2 = __ballot_sync(0xffffffffu, cls == 2);
+                if (lane == 0) {
+                    wc[warp * 3] = __popc(m0);
+                    wc[warp * 3 + 1] = __popc(m1);
+                    wc[warp * 3 + 2] = __popc(m2);
+                }
+                __syncthreads();
+                uint32_t q0 = base0, q1 = base1, q2 = base2;
+                for (int w = 0; w < warp; ++w) {
+                    q0 += wc[w * 3];
+                    q1 += wc[w * 3 + 1];
+                    q2 += wc[w * 3 + 2];
+                }
+                const uint32_t lm = lanemask_lt();
+                if (valid) {
+                    const uint32_t pos = cls == 0 ? q0 + __popc(m0 & lm) : cls == 1 ? q1 + __popc(m1 & lm)
+                                                                                    : q2 + __popc(m2 & lm);
+                    p0[pos] = (uint32_t)i;
+                }
+                for (int w = 0; w < kG2Warps; ++w) {
+                    base0 += wc[w * 3];
+                    base1 += wc[w * 3 + 1];
+                    base2 += wc[w * 3 + 2];
+                }
+                __syncthreads();
+            }
+            __threadfence_block();
+            __syncthreads();
+            // sort the "less" and "greater" parts (the equal part is already id-ordered)
+            const int64_t part_lo[2] = {0, nlt + neq};
+            const int64_t part_len[2] = {nlt, len - nlt - neq};
+            for (int q = 0; q < 2; ++q) {
+                if (part_len[q] <= 1) continue;
+                uint32_t* c = p0 + part_lo[q];
+                cta_lsd<uint32_t, uint32_t>(gk, c, p0 + part_lo[q], p1 + part_lo[q], part_len[q], sh1, varying, wc,
+                                            ws);
+                if (c != p0 + part_lo[q]) {
+                    for (int64_t r = threadIdx.x; r < part_len[q]; r += kG2Threads) p0[part_lo[q] + r] = c[r];
+                    __threadfence_block();
+                    __syncthreads();
+                }
+            }
+            cur = p0;
+        } else {
+            cta_lsd<uint32_t, uint32_t>(gk, cur, p0, p1, len, sh1, varying, wc, ws);
+        }
+    }
+    cta_emit<uint32_t>(gk, gi, cur, len, lo, t, bin, a, ws, &bc);
+}
+
+// Run-length encoding of fully sorted keys (LSD path): chunk c = items
+// [c*kG2Cap, (c+1)*kG2Cap) of a table; heads by comparison with the previous item;
+// bucket numbering by the same chained look-back as the per-chunk sort.
+__global__ void __launch_bounds__(kG2Threads) g3_rle(const uint64_t* __restrict__ keys, int64_t n, int nchunks,
+                                                     unsigned long long* __restrict__ state, IndexDev out) {
+    __shared__ uint32_t ws[32];
+    __shared__ uint32_t bc;
+    constexpr int VP = kG2Cap / kG2Threads;
+    const int t = blockIdx.x, c = blockIdx.y;
+    const uint64_t* k = keys + (int64_t)t * n;
+    const int64_t lo = (int64_t)c * kG2Cap;
+    const int64_t r0 = lo + threadIdx.x * VP;
+    uint64_t kv[VP];
+    uint32_t hm = 0;
+    uint64_t prev = (r0 > 0 && r0 <= n) ? k[r0 - 1] : 0ull;
+#pragma unroll
+    for (int j = 0; j < VP; ++j) {
+        const int64_t r = r0 + j;
+        kv[j] = r < n ? k[r] : 0ull;
+        if (r < n && (r == 0 || kv[j] != prev)) hm |= 1u << j;
+        prev = kv[j];
+    }
+    uint32_t utot;
+    const uint32_t ex = block_excl_scan<kG2Threads>(__popc(hm), ws, &utot);
+    if (threadIdx.x < 32) {
+        const uint32_t pre = chained_prefix_warp(state + (int64_t)t * nchunks, c, utot);
+        if (threadIdx.x == 0) bc = pre;
+    }
+    __syncthreads();
+    const uint32_t base = bc;
+    uint64_t* uk = out.ukeys + (int64_t)t * n;
+    uint32_t* of = out.offs + (int64_t)t * (n + 1);
+    uint32_t ub = base + ex;
+#pragma unroll
+    for (int j = 0; j < VP; ++j)
+        if ((hm >> j) & 1u) {
+            uk[ub] = kv[j];
+            of[ub] = (uint32_t)(r0 + j);
+            ++ub;
+        }
+    if (threadIdx.x == 0 && c == nchunks - 1) {
+        out.nb[t] = base + utot;
+        of[base + utot] = (uint32_t)n;
+    }
+}
+
+static size_t g1_scatter_smem(int nb1) {
+    return (size_t)kG1Tile * 14 + (size_t)nb1 * 8 + (size_t)kG1Warps * nb1 * 2;
+}
+static size_t g2_smem() { return (size_t)kG2Cap * 16 + (size_t)kG2Warps * 256 * 2; }
+
+size_t group_hist_words(int64_t n, int W) {
+    return ((size_t)1 << group_l1_bits(n, W)) * group_tiles(n);
+}
+int group_bins(int64_t n, int W) { return 1 << group_l1_bits(n, W); }
+int group_chunks(int64_t n) { return (int)((n + kG2Span - 1) / kG2Span); }
+size_t group_spec_bytes() { return sizeof(L1Spec); }
+
+// One L1 counting pass (histogram, tile scan, bin starts, stable scatter) of every
+// table by the digit of spec[0..L).
+static cudaError_t l1_pass(const uint64_t* kin, const uint32_t* iin, uint64_t* kout, uint32_t* iout, int64_t n, int L,
+                           const L1Spec* spec, int nb1, uint32_t id_base, GroupScratch& sc, int span, int nchunks,
+                           uint32_t* chunkbin, cudaStream_t s) {
+    const int T = (int)group_tiles(n);
+    const dim3 g1(T, L);
+    timing_begin("group_hist", s);
+    g1_hist<<<g1, kG1Threads, nb1 * sizeof(uint32_t), s>>>(kin, n, spec, nb1, sc.hist, T);
+    count_launch();
+    timing_end("group_hist", s);
+    timing_begin("group_scan", s);
+    const int64_t warps = (int64_t)L * ((nb1 + 31) / 32);
+    g1_scan<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(sc.hist, T, L, nb1, sc.tot);
+    count_launch();
+    g1_binstart<<<L, 1024, 0, s>>>(sc.tot, nb1, n, sc.binstart, span, nchunks, chunkbin);
+    count_launch();
+    timing_end("group_scan", s);
+    timing_begin("group_scatter", s);
+    const size_t sm1 = g1_scatter_smem(nb1);
+    cudaError_t e;
+    if (iin == nullptr) {
+        e = cudaFuncSetAttribute(g1_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+        if (e != cudaSuccess) return e;
+        g1_scatter<true><<<g1, kG1Threads, sm1, s>>>(kin, nullptr, kout, iout, n, spec, nb1, sc.hist, sc.binstart, T,
+                                                     id_base);
+    } else {
+        e = cudaFuncSetAttribute(g1_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+        if (e != cudaSuccess) return e;
+        g1_scatter<false><<<g1, kG1Threads, sm1, s>>>(kin, iin, kout, iout, n, spec, nb1, sc.hist, sc.binstart, T,
+                                                      id_base);
+    }
+    count_launch();
+    timing_end("group_scatter", s);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_base, int W, GroupScratch& sc,
                          IndexDev& out, int* flags, cudaStream_t s) {
+    (void)flags;
     cudaError_t e;
     if (n == 0) {
         e = cudaMemsetAsync(out.nb, 0, sizeof(uint32_t) * L, s);
         if (e != cudaSuccess) return e;
         return cudaMemsetAsync(out.offs, 0, sizeof(uint32_t) * L * (n + 1), s);
     }
-    const int T = (int)group_tiles(n);
-    const dim3 g2(T, L);
-    // digit shifts covering the top 16 significant bits, low digit first
-    int shifts[2];
-    int npass;
-    if (W <= 8) {
-        shifts[0] = 0;
-        npass = 1;
-    } else if (W <= 16) {
-        shifts[0] = 0;
-        shifts[1] = 8;
-        npass = 2;
-    } else {
-        shifts[0] = W - 16;
-        shifts[1] = W - 8;
-        npass = 2;
-    }
-    // pass outputs alternate keys_a, keys_b (keys_b may alias the input keys:
-    // the input is fully consumed by pass 0, which writes keys_a)
-    const uint64_t* kin = keys;
-    const uint32_t* iin = nullptr;
-    for (int p = 0; p < npass; ++p) {
-        const bool lastp = (p == npass - 1);
-        uint64_t* kout = (p == 0) ? sc.keys_a : sc.keys_b;
-        uint32_t* iout = lastp ? out.ids : sc.ids_a;
-        timing_begin("radix_upsweep", s);
-        if (p == 0) radix_upsweep<true><<<g2, kRT, 0, s>>>(kin, n, shifts[p], sc.hist, T);
-        else radix_upsweep<false><<<g2, kRT, 0, s>>>(kin, n, shifts[p], sc.hist, T);
-        count_launch();
-        timing_end("radix_upsweep", s);
-        timing_begin("radix_scan", s);
-        scan_rows<<<L, 1024, 0, s>>>(sc.hist, (int64_t)256 * T, (int64_t)256 * T, nullptr, 0);
-        count_launch();
-        timing_end("radix_scan", s);
-        timing_begin("radix_downsweep", s);
-        const int dsm = kTile * 12;
-        if (p == 0) {
-            cudaFuncSetAttribute(radix_downsweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm);
-            radix_downsweep<true><<<g2, kRT, dsm, s>>>(kin, iin, kout, iout, n, shifts[p], sc.hist, T, id_base);
-        } else {
-            cudaFuncSetAttribute(radix_downsweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm);
-            radix_downsweep<false><<<g2, kRT, dsm, s>>>(kin, iin, kout, iout, n, shifts[p], sc.hist, T, id_base);
-        }
-        count_launch();
-        timing_end("radix_downsweep", s);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        kin = kout;
-        iin = iout;
-    }
-    uint64_t* sorted = (npass == 1) ? sc.keys_a : sc.keys_b;
-    if (W > 16) {
-        timing_begin("segsort", s);
-        e = cudaMemsetAsync(sc.overflow, 0, sizeof(uint32_t), s);
+    L1Spec* spec = reinterpret_cast<L1Spec*>(sc.spec);
+    const bool lsd = group_is_lsd(W);
+    const int B1 = group_l1_bits(n, W);
+    const int nb1 = 1 << B1;
+    timing_begin("group_hist", s);
+    e = cudaMemsetAsync(sc.vmask, 0, sizeof(unsigned long long) * 2 * L, s);
+    if (e != cudaSuccess) return e;
+    g0_mask<<<dim3((unsigned)((n + 8191) / 8192), L), 256, 0, s>>>(keys, n, sc.vmask);
+    count_launch();
+    g0_spec<<<(L + 127) / 128, 128, 0, s>>>(sc.vmask, L, B1, lsd ? 2 : 1, spec);
+    count_launch();
+    timing_end("group_hist", s);
+    if (lsd) {
+        // narrow keys: full stable LSD sort on the varying bits (two passes), then RLE
+        e = l1_pass(keys, nullptr, sc.keys_a, sc.ids_a, n, L, spec, nb1, id_base, sc, 0, 0, nullptr, s);
         if (e != cudaSuccess) return e;
-        const dim3 gw((unsigned)((n + kSegWin - 1) / kSegWin), L);
-        segsort_window<<<gw, 256, 0, s>>>(sorted, out.ids, n, W - 16, sc.overflow, sc.overflow_cap);
+        uint64_t* kb = reinterpret_cast<uint64_t*>(sc.perm);
+        e = l1_pass(sc.keys_a, sc.ids_a, kb, out.ids, n, L, spec + L, nb1, id_base, sc, 0, 0, nullptr, s);
+        if (e != cudaSuccess) return e;
+        const int nch = (int)((n + kG2Cap - 1) / kG2Cap);
+        timing_begin("group_sort", s);
+        e = cudaMemsetAsync(sc.state, 0, sizeof(unsigned long long) * (size_t)L * nch, s);
+        if (e != cudaSuccess) return e;
+        g3_rle<<<dim3(L, nch), kG2Threads, 0, s>>>(kb, n, nch, sc.state, out);
         count_launch();
-        timing_end("segsort", s);
-        timing_begin("segsort_long", s);
-        const size_t smem = kSegBig * (sizeof(uint64_t) + sizeof(uint32_t));
-        cudaFuncSetAttribute(segsort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        // scratch for long segments: the pass-0 buffers are free once pass 1 has run
-        segsort_big<<<148, 1024, smem, s>>>(sorted, out.ids, sc.keys_a, sc.ids_a, n, W - 16, sc.overflow,
-                                            sc.overflow_cap, flags);
-        count_launch();
-        timing_end("segsort_long", s);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        timing_end("group_sort", s);
+        return cudaGetLastError();
     }
-    timing_begin("rle", s);
-    rle_count<<<g2, kRT, 0, s>>>(sorted, n, sc.tile_aux, T);
+    const int nch = group_chunks(n);
+    e = l1_pass(keys, nullptr, sc.keys_a, sc.ids_a, n, L, spec, nb1, id_base, sc, kG2Span, nch, sc.chunkbin, s);
+    if (e != cudaSuccess) return e;
+    timing_begin("group_sort", s);
+    e = cudaMemsetAsync(sc.state, 0, sizeof(unsigned long long) * (size_t)L * nch, s);
+    if (e != cudaSuccess) return e;
+    G2Args a;
+    a.keys = sc.keys_a;
+    a.ids = sc.ids_a;
+    a.binstart = sc.binstart;
+    a.state = sc.state;
+    a.scratch = sc.perm;
+    a.spec = spec;
+    a.n = n;
+    a.nb1 = nb1;
+    a.nchunks = nch;
+    a.chunkbin = sc.chunkbin;
+    a.out = out;
+    const size_t sm2 = g2_smem();
+    e = cudaFuncSetAttribute(g2_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+    if (e != cudaSuccess) return e;
+    g2_sort<<<dim3(L, nch), kG2Threads, sm2, s>>>(a);
     count_launch();
-    scan_rows<<<L, 1024, 0, s>>>(sc.tile_aux, T, T + 1, nullptr, 1);
-    count_launch();
-    rle_write<<<g2, kRT, 0, s>>>(sorted, n, sc.tile_aux, T, out);
-    count_launch();
-    rle_finish<<<(L + 127) / 128, 128, 0, s>>>(out, sc.tile_aux, T, n, L);
-    count_launch();
-    timing_end("rle", s);
+    timing_end("group_sort", s);
     return cudaGetLastError();
 }
 

@@ -88,14 +88,16 @@ cudaError_t launch_keys_from_proj(const float* Y, int64_t n, int m, int L, int K
 
 // Grouping.
 struct GroupScratch {
-    uint64_t* keys_a;
-    uint64_t* keys_b;
-    uint32_t* ids_a;
-    uint32_t* ids_b;
-    uint32_t* hist;       // [L][256][tiles] (reused per pass)
-    uint32_t* tile_aux;   // [L][tiles+1]
-    uint32_t* overflow;   // [1 + 3 * cap] (count, then (t, lo, hi) triples)
-    int overflow_cap;
+    uint64_t* keys_a;           // [L][n] keys after the L1 scatter
+    uint32_t* ids_a;            // [L][n] ids after the L1 scatter
+    uint32_t* hist;             // [L][nb1][tiles] per-tile L1 digit counts, then their tile scan
+    uint32_t* tot;              // [L][nb1] bin totals
+    uint32_t* binstart;         // [L][nb1+1]
+    unsigned long long* state;  // [L][chunks] look-back words of the per-chunk kernel
+    uint32_t* perm;             // [L][2n] permutation scratch for bins larger than shared memory
+    unsigned long long* vmask;  // [L][2] OR of keys, OR of complemented keys
+    void* spec;                 // [2][L] L1 digit specs (group.cu)
+    uint32_t* chunkbin;         // [L][chunks+1] first L1 bin of every L2 chunk
 };
 struct IndexDev {
     uint32_t* ids;    // [L][n]
@@ -104,6 +106,11 @@ struct IndexDev {
     uint32_t* nb;     // [L]
 };
 size_t group_tiles(int64_t n);
+int group_bins(int64_t n, int key_width);
+size_t group_hist_words(int64_t n, int key_width);
+size_t group_spec_bytes();
+int group_chunks(int64_t n);
+bool group_is_lsd(int key_width);
 cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_base, int key_width,
                          GroupScratch& sc, IndexDev& out, int* flags, cudaStream_t s);
 cudaError_t launch_lookup(const uint64_t* qkeys, int64_t nq, int L, int64_t n, const IndexDev& idx,

@@ -320,3 +320,53 @@ def test_group_long_equal_prefix_segments():
     idx = h.group_keys(torch.from_numpy(keys.view(np.int64)).cuda().view(torch.uint64), id_base=5)
     _check_index(idx, lsh.group(keys, id_base=5), 2)
     h.check()
+
+
+def _structured_keys(kind: str, L: int, n: int, g) -> np.ndarray:
+    u64 = np.uint64
+    if kind == "uniform":
+        return g.integers(0, 2 ** 63, (L, n), dtype=np.int64).astype(u64) * u64(2) + g.integers(0, 2, (L, n)).astype(u64)
+    if kind == "smem_long_segments":
+        # inside one L1 bin: > 64 keys sharing the next 16 bits but differing below (and duplicates)
+        k = _structured_keys("uniform", L, n, g)
+        pref = u64(0x5A5A5) << u64(44)
+        k[:, 100:700] = pref | g.integers(0, 40, (L, 600)).astype(u64) << u64(3)
+        k[:, 900:1000] = pref | u64(7)
+        return k
+    if kind == "big_bin_no_dominant":
+        # one L1 bin far larger than shared memory, keys spread (no 3-way split)
+        k = g.integers(0, 2 ** 62, (L, n), dtype=np.int64).astype(u64)
+        k[:, : n // 2] = (u64(3) << u64(60)) | g.integers(0, 2 ** 20, (L, n // 2)).astype(u64) << u64(7)
+        return k
+    if kind == "all_equal":
+        return np.full((L, n), 0xDEADBEEF12345678, dtype=u64)
+    if kind == "two_values":
+        return np.where(g.integers(0, 2, (L, n)) == 1, u64(2 ** 63 + 5), u64(5)).astype(u64)
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("kind,n", [("uniform", 4097), ("uniform", 300001), ("smem_long_segments", 6000),
+                                    ("big_bin_no_dominant", 40000), ("all_equal", 20000), ("two_values", 9000)])
+def test_group_keys_structures(kind, n):
+    """L1 MSD scatter + per-bin sort paths: shared-memory bins with long equal-prefix
+    segments, bins larger than shared memory with and without a dominant key, ragged tiles."""
+    L = 3
+    p = lsh.Params("CS_E2LSH", d=64, m=L * 16, L=L, K=16, w=4.0, seed=0)
+    h = _handle(p)
+    keys = _structured_keys(kind, L, n, np.random.default_rng(n))
+    idx = h.group_keys(torch.from_numpy(keys.view(np.int64)).cuda().view(torch.uint64), id_base=3)
+    _check_index(idx, lsh.group(keys, id_base=3), L)
+    h.check()
+
+
+@pytest.mark.parametrize("K,n", [(1, 5000), (3, 70000), (11, 100000), (40, 30000)])
+def test_group_keys_srp_widths(K, n):
+    """SRP keys are K bits wide: the L1 digit never exceeds the key width."""
+    L = 2
+    p = lsh.Params("CS_SRP", d=64, m=L * K, L=L, K=K, w=4.0, seed=0)
+    h = _handle(p)
+    g = np.random.default_rng(K)
+    keys = g.integers(0, 2 ** min(K, 62), (L, n), dtype=np.int64).astype(np.uint64)
+    keys[:, ::5] = keys[0, 0]
+    idx = h.group_keys(torch.from_numpy(keys.view(np.int64)).cuda().view(torch.uint64), id_base=0)
+    _check_index(idx, lsh.group(keys, id_base=0), L)

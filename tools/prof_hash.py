@@ -36,7 +36,7 @@ for i in range(1 + a.reps):
     else:
         idx = h.build_index(X)
 torch.cuda.synchronize()
-for k in ("sketch", "radix_upsweep", "radix_scan", "radix_downsweep", "segsort", "segsort_long", "rle", "dense_gemm",
+for k in ("sketch", "group_hist", "group_scan", "group_scatter", "group_sort", "dense_gemm",
           "keys_from_proj"):
     ms, cnt = pk.timing_get(k)
     if cnt:

@@ -26,5 +26,5 @@ for _ in range(a.steps):
     keep.append(idx)
     if len(keep) > a.keep: keep.pop(0)
 e1.record(); t1 = time.perf_counter(); torch.cuda.synchronize(); t2 = time.perf_counter()
-tot = sum(pk.timing_get(k)[0] for k in ("sketch", "sketch_query", "radix_upsweep", "radix_scan", "radix_downsweep", "segsort", "rle", "lookup"))
+tot = sum(pk.timing_get(k)[0] for k in ("sketch", "sketch_query", "group_hist", "group_scan", "group_scatter", "group_sort", "lookup"))
 print(f"{a.scheme} device {e0.elapsed_time(e1)/a.steps:.3f} ms/step  kernels {tot/a.steps:.3f} ms/step  host enqueue {1e3*(t1-t0)/a.steps:.3f} ms/step  wall {1e3*(t2-t0)/a.steps:.3f}")
