@@ -270,6 +270,9 @@ struct lsh_handle {
     std::vector<int32_t*> d_h, d_s;
     float* d_b = nullptr;
     bool sketch_ok = true;
+    bool hcs = false;          // HCS slab plan available (sketch_hcs.cu)
+    HcsPlanDev hplan{};
+    void* d_hplan_mem = nullptr;
 };
 
 struct lsh_index {
@@ -398,6 +401,113 @@ static lsh_status build_chunked_plan(lsh_handle* H, const std::vector<int32_t>& 
     return LSH_OK;
 }
 
+// HCS slab plan (sketch_hcs.cu): slab = the d_1*d_2 contiguous inputs of one outer
+// index J = (i_3..i_N); all slabs share the slab-internal bin map (h_1 + m_1 h_2,
+// s_1 s_2) and add into the block g(J) of m_1*m_2 bins with sign s(J).  Built in
+// addition to the generic plan, which stays the fallback for unaligned inputs.
+static lsh_status build_hcs_plan(lsh_handle* H) {
+    const lsh_params* p = &H->p;
+    const HostTables& t = H->host;
+    if (!is_hcs(p->scheme) || t.N < 3) return LSH_OK;
+    const int64_t S64 = t.md[0] * t.md[1], M64 = t.mm[0] * t.mm[1];
+    if (S64 > 1024 || M64 > 1024) return LSH_OK;
+    const int S = (int)S64, M12 = (int)M64;
+    if (!hcs_plan_supported(S, M12) || M12 % p->K != 0 || p->d % S != 0) return LSH_OK;
+    if (hcs_smem_bytes(S, M12, p->m, (int)(p->d / S + p->m / M12) + 4, 0) > 232448) return LSH_OK;
+    if (p->d / S > 0x7fffffff) return LSH_OK;
+    std::vector<int> bin12(S);
+    std::vector<uint32_t> sgn((S + 31) / 32, 0);
+    for (int k = 0; k < S; ++k) {
+        const int i1 = k % (int)t.md[0], i2 = k / (int)t.md[0];
+        bin12[k] = t.h[0][i1] + (int)t.mm[0] * t.h[1][i2];
+        if (t.s[0][i1] * t.s[1][i2] < 0) sgn[k >> 5] |= 1u << (k & 31);
+    }
+    // pos[q] = staged word offset (sketch_hcs.cu layout) of the coordinate at
+    // bin-sorted position q; bp = bin starts in that order
+    std::vector<uint16_t> bp(M12 + 1, 0), pos(S);
+    for (int k = 0; k < S; ++k) bp[bin12[k] + 1]++;
+    for (int b = 0; b < M12; ++b) bp[b + 1] += bp[b];
+    {
+        std::vector<uint16_t> cur(bp.begin(), bp.end() - 1);
+        for (int k = 0; k < S; ++k) pos[cur[bin12[k]]++] = (uint16_t)((k >> 2) * 129 + (k & 3) * 32);
+    }
+    // bins -> 16 warps, M12/16 each, greedy by coordinate count (largest first) so the
+    // per-slab gather work of the warps is balanced
+    const int bpw = M12 / 16;
+    std::vector<uint8_t> wbins(M12);
+    {
+        std::vector<int> order(M12), load(16, 0), nb(16, 0);
+        for (int b = 0; b < M12; ++b) order[b] = b;
+        std::stable_sort(order.begin(), order.end(),
+                         [&](int a, int b) { return bp[a + 1] - bp[a] > bp[b + 1] - bp[b]; });
+        for (int b : order) {
+            int best = -1;
+            for (int w = 0; w < 16; ++w)
+                if (nb[w] < bpw && (best < 0 || load[w] < load[best])) best = w;
+            wbins[best * bpw + nb[best]++] = (uint8_t)b;
+            load[best] += bp[b + 1] - bp[b];
+        }
+    }
+    const int64_t nslab = p->d / S;
+    const int nblocks = p->m / M12;
+    std::vector<std::vector<std::pair<uint32_t, bool>>> lists(nblocks);
+    for (int64_t J = 0; J < nslab; ++J) {
+        int64_t rem = J, g = 0, stride = 1;
+        int sg = 1;
+        for (int k = 2; k < t.N; ++k) {
+            const int64_t ik = rem % t.md[k];
+            rem /= t.md[k];
+            g += (int64_t)t.h[k][ik] * stride;
+            stride *= t.mm[k];
+            sg *= t.s[k][ik];
+        }
+        lists[g].push_back({(uint32_t)J, sg < 0});
+    }
+    std::vector<uint2> ents;
+    std::vector<int32_t> bfirst(nblocks);
+    for (int g = 0; g < nblocks; ++g) {
+        bfirst[g] = (int32_t)ents.size();
+        if (lists[g].empty()) {
+            ents.push_back(make_uint2(0u, (uint32_t)g | HCS_EMPTY | HCS_LAST));
+            continue;
+        }
+        for (size_t i = 0; i < lists[g].size(); ++i) {
+            uint32_t y = (uint32_t)g;
+            if (lists[g][i].second) y |= HCS_NEG;
+            if (i + 1 == lists[g].size()) y |= HCS_LAST;
+            ents.push_back(make_uint2(lists[g][i].first, y));
+        }
+    }
+    while (ents.size() % 4) ents.push_back(make_uint2(0u, HCS_EMPTY));   // pad to whole steps (no block)
+    const size_t b_e = sizeof(uint2) * ents.size(), b_p = sizeof(uint16_t) * S, b_s = sizeof(uint32_t) * sgn.size(),
+                 b_b = sizeof(uint16_t) * bp.size(), b_f = sizeof(int32_t) * bfirst.size(), b_w = wbins.size();
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    CK(cudaMalloc(&H->d_hplan_mem, al(b_e) + al(b_p) + al(b_s) + al(b_b) + al(b_f) + al(b_w)));
+    char* base = (char*)H->d_hplan_mem;
+    CK(cudaMemcpy(base, ents.data(), b_e, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(base + al(b_e), pos.data(), b_p, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(base + al(b_e) + al(b_p), sgn.data(), b_s, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(base + al(b_e) + al(b_p) + al(b_s), bp.data(), b_b, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(base + al(b_e) + al(b_p) + al(b_s) + al(b_b), bfirst.data(), b_f, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(base + al(b_e) + al(b_p) + al(b_s) + al(b_b) + al(b_f), wbins.data(), b_w, cudaMemcpyHostToDevice));
+    HcsPlanDev hp{};
+    hp.m = p->m;
+    hp.K = p->K;
+    hp.S = S;
+    hp.M12 = M12;
+    hp.nentries = (int)ents.size();
+    hp.entries = (const uint2*)base;
+    hp.pos = (const uint16_t*)(base + al(b_e));
+    hp.sgn = (const uint32_t*)(base + al(b_e) + al(b_p));
+    hp.bp = (const uint16_t*)(base + al(b_e) + al(b_p) + al(b_s));
+    hp.nblocks = nblocks;
+    hp.bfirst = (const int32_t*)(base + al(b_e) + al(b_p) + al(b_s) + al(b_b));
+    hp.wbins = (const uint8_t*)(base + al(b_e) + al(b_p) + al(b_s) + al(b_b) + al(b_f));
+    H->hplan = hp;
+    H->hcs = true;
+    return LSH_OK;
+}
+
 static lsh_status build_plan(lsh_handle* H) {
     const lsh_params* p = &H->p;
     std::vector<int32_t> bin;
@@ -451,6 +561,7 @@ static void free_handle(lsh_handle* H) {
     cudaFree(H->d_entries);
     cudaFree(H->d_binptr);
     cudaFree(H->d_cplan_mem);
+    cudaFree(H->d_hplan_mem);
     cudaFree(H->d_signs);
     cudaFree(H->d_pairs);
     cudaFree(H->d_bigmask);
@@ -530,6 +641,7 @@ extern "C" lsh_status lsh_create(const lsh_params* p, lsh_handle** out) {
             cudaMemcpy(ds, H->host.s[k].data(), bytes, cudaMemcpyHostToDevice);
         }
         st = build_plan(H);
+        if (st == LSH_OK) st = build_hcs_plan(H);
         if (st != LSH_OK) return fail(st);
     }
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail(cuda_fail(e, "create sync"));
@@ -592,10 +704,17 @@ static lsh_status hash_impl(const lsh_handle* H, const float* X, int64_t n, int6
         if (!out.proj) CK(cudaFreeAsync(Y, s));
         return LSH_OK;
     }
-    if (!H->sketch_ok) return LSH_EUNSUPPORTED;
+    if (!H->sketch_ok && !H->hcs) return LSH_EUNSUPPORTED;
     timing_begin(tname, s);
-    cudaError_t e = H->chunked ? launch_sketch_chunked(H->cplan, H->disc, X, n, ld, out, H->num_sms, s)
-                               : launch_sketch(H->plan, H->disc, X, n, ld, out, H->num_sms, s);
+    const bool hcs_vec = H->hcs && (ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0) &&
+                         !(getenv("LSH_NO_HCS_SLAB") && getenv("LSH_NO_HCS_SLAB")[0] == '1');
+    if (!hcs_vec && !H->sketch_ok) {
+        timing_end(tname, s);
+        return LSH_EUNSUPPORTED;
+    }
+    cudaError_t e = hcs_vec      ? launch_sketch_hcs(H->hplan, H->disc, X, n, ld, out, H->num_sms, s)
+                    : H->chunked ? launch_sketch_chunked(H->cplan, H->disc, X, n, ld, out, H->num_sms, s)
+                                 : launch_sketch(H->plan, H->disc, X, n, ld, out, H->num_sms, s);
     count_launch();
     timing_end(tname, s);
     if (e != cudaSuccess) return cuda_fail(e, "sketch");

@@ -56,6 +56,25 @@ struct ChunkedPlanDev {
     const uint8_t* cnt;      // coordinates per bin in the chunk (saturated at 255)
 };
 
+// HCS slab plan (sketch_hcs.cu): slab = d_1*d_2 contiguous inputs (one outer index
+// J = (i_3..i_N)), adding into one block of M12 = m_1*m_2 bins; entries list the
+// slabs block by block (empty blocks get one EMPTY entry).
+#define HCS_BLOCK_MASK 0x1fffffffu
+#define HCS_EMPTY (1u << 29)
+#define HCS_NEG (1u << 30)
+#define HCS_LAST (1u << 31)
+struct HcsPlanDev {
+    int m, K, S, M12;
+    int nentries;
+    const uint2* entries;    // .x = slab index J (input offset J*S), .y = block | flags
+    const uint16_t* pos;     // [S] staged word offset of the coordinate at each bin-sorted position
+    const uint32_t* sgn;     // [S/32] slab-internal sign bits (s_1 s_2 = -1)
+    const uint16_t* bp;      // [M12+1] bin starts in the slab's bin-sorted order
+    const uint8_t* wbins;    // [16][M12/16] bins of each warp (balanced by coordinate count)
+    int nblocks;             // m / M12
+    const int32_t* bfirst;   // [nblocks] index of each block's first entry
+};
+
 struct DiscretizeDev {
     int e2lsh;                // 1: E2LSH floor codes + fingerprint keys; 0: SRP bits
     float c_scale;            // sqrt(m)/w (CS/HCS), 1/w (dense)
@@ -77,6 +96,10 @@ size_t sketch_smem_bytes(int Q, int m, int d, int L);
 cudaError_t launch_sketch_chunked(const ChunkedPlanDev& plan, const DiscretizeDev& disc, const float* X, int64_t n,
                                   int64_t ld, HashOut out, int num_sms, cudaStream_t s);
 size_t chunked_smem_bytes(int m, int gbins);
+cudaError_t launch_sketch_hcs(const HcsPlanDev& plan, const DiscretizeDev& disc, const float* X, int64_t n,
+                              int64_t ld, HashOut out, int num_sms, cudaStream_t s);
+size_t hcs_smem_bytes(int S, int M12, int m, int nentries, int nst);
+bool hcs_plan_supported(int S, int M12);
 
 cudaError_t launch_dense_gemm_f32(const float* X, int64_t n, int64_t ld, const uint16_t* Rbf16, int m, int d,
                                   float* Y, cudaStream_t s);
