@@ -802,6 +802,7 @@ static lsh_status group_impl(const lsh_handle* H, const uint64_t* keys, uint64_t
         sc.spec = take(b_spec);
         sc.chunkbin = (uint32_t*)take(b_cb);
     }
+    sc.num_sms = H->num_sms;
     cudaError_t e = launch_group(keys, n, L, (uint32_t)id_base, H->key_width, sc, I->dev, H->d_flags, s);
     if (e != cudaSuccess) return cuda_fail(e, "group");
     if (mem) CK(cudaFreeAsync(mem, s));

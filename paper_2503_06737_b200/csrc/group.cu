@@ -24,11 +24,13 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "internal.hpp"
 
 namespace lshb {
 
-constexpr int kG1Tile = 4096;                   // items per L1 tile
+constexpr int kG1Tile = 8192;                   // items per L1 tile
 constexpr int kG1Threads = 256;
 constexpr int kG1Warps = kG1Threads / 32;       // 8
 constexpr int kG1PerWarp = kG1Tile / kG1Warps;  // 512 consecutive items per warp
@@ -58,6 +60,23 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t r;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
     return r;
+}
+
+// Lanes of the warp holding the same digit (digits < 2^NB; invalid lanes match only
+// themselves): one ballot per digit bit instead of match.any, whose cost grows with
+// the number of distinct values (about 32 here).
+template <int NB>
+__device__ __forceinline__ uint32_t match_digit(uint32_t d, int nbits, bool valid) {
+    uint32_t m = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        if (b < nbits) {
+            const bool bit = (d >> b) & 1u;
+            const uint32_t bb = __ballot_sync(0xffffffffu, bit);
+            m &= bit ? bb : ~bb;
+        }
+    }
+    return valid ? m : (1u << (threadIdx.x & 31));
 }
 
 // Exclusive block scan of one value per thread (NT threads); optional total.
@@ -186,17 +205,21 @@ __global__ void __launch_bounds__(kG1Threads) g1_hist(const uint64_t* __restrict
     const uint64_t* kt = keys + (int64_t)t * n + t0;
     const int cn = (int)min((int64_t)kG1Tile, n - t0);
     const L1Spec sp = spec[t];
-    uint64_t k[kG1Tile / kG1Threads];
+    constexpr int R = 16;   // keys per thread per batch
+#pragma unroll 1
+    for (int b0 = 0; b0 < kG1Tile; b0 += R * kG1Threads) {
+        uint64_t k[R];
 #pragma unroll
-    for (int r = 0; r < kG1Tile / kG1Threads; ++r) {
-        const int i = r * kG1Threads + threadIdx.x;
-        k[r] = i < cn ? __ldcs(kt + i) : 0ull;
-    }
-    __syncthreads();
+        for (int r = 0; r < R; ++r) {
+            const int i = b0 + r * kG1Threads + threadIdx.x;
+            k[r] = i < cn ? __ldcs(kt + i) : 0ull;
+        }
+        if (b0 == 0) __syncthreads();   // counters cleared
 #pragma unroll
-    for (int r = 0; r < kG1Tile / kG1Threads; ++r) {
-        const int i = r * kG1Threads + threadIdx.x;
-        if (i < cn) atomicAdd(&g1_cnt[l1_digit(k[r], sp)], 1u);
+        for (int r = 0; r < R; ++r) {
+            const int i = b0 + r * kG1Threads + threadIdx.x;
+            if (i < cn) atomicAdd(&g1_cnt[l1_digit(k[r], sp)], 1u);
+        }
     }
     __syncthreads();
     uint32_t* row = hist + ((int64_t)t * T + tile) * nb1;
@@ -262,107 +285,183 @@ __global__ void __launch_bounds__(1024) g1_binstart(const uint32_t* __restrict__
     if (threadIdx.x == 0) cb[nchunks] = (uint32_t)nb1;
 }
 
-// Stable scatter of one 4096-item tile by its L1 digit.  Warp w owns items
-// [512w, 512w+512) of the tile (coalesced 32-item rounds) and ranks them with
-// match_any against warp-private running digit counts; one block pass turns
-// (digit, warp) counts into offsets; items are staged in digit order in shared
-// memory and written so that consecutive threads write consecutive addresses.
+// Stable scatter by the L1 digit, persistent: CTA c takes work items c, c + grid, ...
+// (item = (table, 4096-key tile), table-major so that the CTAs in flight scatter into
+// one table's destination, which stays resident in L2).  A tile's keys are 32 KB
+// contiguous: one bulk async copy (cp.async.bulk + mbarrier) per tile into a ring of
+// NST shared-memory stages, issued NST-1 tiles ahead, so no thread waits on DRAM.
+// Ranking: warp w owns items [256w, 256w+256) in 8 coalesced rounds; match_any gives
+// the rank among equal digits in a round, warp-private running counts order the
+// rounds, one block pass turns (digit, warp) counts into offsets.  The write-out goes
+// through a u16 permutation so consecutive threads write consecutive addresses.
+namespace {
+__device__ __forceinline__ uint32_t g_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void g_mbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(g_smem_u32(bar)));
+}
+__device__ __forceinline__ void g_mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(g_smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void g_mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "LAB_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra LAB_WAIT_%=;\n"
+        "}\n" ::"r"(g_smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void g_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(g_smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(g_smem_u32(bar))
+        : "memory");
+}
+}  // namespace
+
+constexpr int kSThreads = 512;
+constexpr int kSWarps = kSThreads / 32;
+constexpr int kSRounds = kG1Tile / kSThreads;   // 16
+
+size_t g1_scatter_smem(int nb1, bool ids, int nst) {
+    (void)ids;
+    return 64 + (size_t)nst * kG1Tile * 8 + (size_t)kG1Tile * 4 + (size_t)nb1 * 8 + (size_t)kSWarps * nb1 * 2;
+}
+
 template <bool IMPLICIT_IDS>
-__global__ void __launch_bounds__(kG1Threads, 3)
+__global__ void __launch_bounds__(kSThreads, 1)
     g1_scatter(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ iin, uint64_t* __restrict__ kout,
                uint32_t* __restrict__ iout, int64_t n, const L1Spec* __restrict__ spec, int nb1,
-               const uint32_t* __restrict__ hist,
-               const uint32_t* __restrict__ binstart, int T, uint32_t id_base) {
-    extern __shared__ __align__(16) unsigned char g1_dsm[];
-    uint64_t* sk = reinterpret_cast<uint64_t*>(g1_dsm);                 // [kG1Tile]
-    uint32_t* si = reinterpret_cast<uint32_t*>(g1_dsm + kG1Tile * 8);   // [kG1Tile]
-    uint32_t* gpos = reinterpret_cast<uint32_t*>(g1_dsm + kG1Tile * 12);  // [nb1] global start of the tile's run
-    uint32_t* loc = gpos + nb1;                                         // [nb1] staged start of the digit
-    uint16_t* sd = reinterpret_cast<uint16_t*>(loc + nb1);              // [kG1Tile] staged digit
-    uint16_t* wrun = sd + kG1Tile;                                      // [kG1Warps][nb1]
+               const uint32_t* __restrict__ hist, const uint32_t* __restrict__ binstart, int T, int L,
+               uint32_t id_base, int nst) {
+    extern __shared__ __align__(128) unsigned char g1_dsm[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(g1_dsm);                                  // [nst]
+    uint64_t* rk = reinterpret_cast<uint64_t*>(g1_dsm + 64);                               // [nst][4096]
+    uint16_t* sp = reinterpret_cast<uint16_t*>(rk + (size_t)nst * kG1Tile);                // staged item
+    uint16_t* sd = sp + kG1Tile;                                                           // staged digit
+    uint32_t* gpos = reinterpret_cast<uint32_t*>(sd + kG1Tile);                            // [nb1]
+    uint32_t* loc = gpos + nb1;                                                            // [nb1]
+    uint16_t* wrun = reinterpret_cast<uint16_t*>(loc + nb1);                               // [kSWarps][nb1]
     __shared__ uint32_t ws[32];
-    const int t = blockIdx.y, tile = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const L1Spec sp = spec[t];
-    for (int i = threadIdx.x; i < kG1Warps * nb1; i += kG1Threads) wrun[i] = 0;
-    const int64_t tb = (int64_t)t * n;
-    const int64_t base = (int64_t)tile * kG1Tile + warp * kG1PerWarp;
-    uint64_t key[kG1Rounds];
-    uint32_t slot[kG1Rounds];
-#pragma unroll
-    for (int r = 0; r < kG1Rounds; ++r) {
-        const int64_t i = base + r * 32 + lane;
-        key[r] = i < n ? __ldcs(kin + tb + i) : 0ull;
+    const int64_t items = (int64_t)T * L;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < nst; ++i) g_mbar_init(bars + i);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    uint16_t* my = wrun + warp * nb1;
-    // all digit matches first (independent, pipelined), then the ordered running counts
-    uint32_t peers[kG1Rounds];
+    // bulk copies need 16-byte aligned, 16-byte multiple ranges: full tiles of tables
+    // whose base is 16-byte aligned; other tiles are loaded by all threads after the wait
+    auto bulk_ok = [&](int t, int tile) {
+        const int64_t cnt = min((int64_t)kG1Tile, n - (int64_t)tile * kG1Tile);
+        const uint64_t a = reinterpret_cast<uint64_t>(kin + (int64_t)t * n + (int64_t)tile * kG1Tile);
+        return cnt == kG1Tile && (a & 15) == 0;
+    };
+    auto issue = [&](int64_t it) {  // thread 0
+        const int64_t w = (int64_t)blockIdx.x + it * gridDim.x;
+        if (w >= items) return;
+        const int st = (int)(it % nst);
+        const int t = (int)(w / T), tile = (int)(w % T);
+        if (!bulk_ok(t, tile)) {
+            g_mbar_arrive_tx(bars + st, 0u);
+            return;
+        }
+        const int64_t off = (int64_t)t * n + (int64_t)tile * kG1Tile;
+        g_mbar_arrive_tx(bars + st, kG1Tile * 8u);
+        g_bulk(rk + (size_t)st * kG1Tile, kin + off, kG1Tile * 8u, bars + st);
+    };
+    if (threadIdx.x == 0)
+        for (int i = 0; i < nst - 1; ++i) issue(i);
+
+    for (int64_t it = 0;; ++it) {
+        const int64_t w = (int64_t)blockIdx.x + it * gridDim.x;
+        if (w >= items) break;
+        const int st = (int)(it % nst);
+        const int t = (int)(w / T), tile = (int)(w % T);
+        const L1Spec sp0 = spec[t];
+        const int nbits1 = sp0.nbits;
+        const int64_t tb = (int64_t)t * n;
+        const int cnt = (int)min((int64_t)kG1Tile, n - (int64_t)tile * kG1Tile);
+        uint64_t* kr = rk + (size_t)st * kG1Tile;
+        const uint32_t* ir = IMPLICIT_IDS ? nullptr : iin + tb + (int64_t)tile * kG1Tile;
+        g_mbar_wait(bars + st, (uint32_t)((it / nst) & 1));
+        for (int i = threadIdx.x; i < kSWarps * nb1; i += kSThreads) wrun[i] = 0;
+        if (!bulk_ok(t, tile)) {
+            for (int i = threadIdx.x; i < cnt; i += kSThreads) kr[i] = kin[tb + (int64_t)tile * kG1Tile + i];
+        }
+        __syncthreads();   // tile in smem; previous write-out finished with its stage
+        if (threadIdx.x == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(it + nst - 1);   // into the stage the previous item used
+        }
+        uint16_t* my = wrun + warp * nb1;
+        uint32_t slot[kSRounds], peers[kSRounds];
+        const int base = warp * (kG1Tile / kSWarps);
 #pragma unroll
-    for (int r = 0; r < kG1Rounds; ++r) {
-        const int64_t i = base + r * 32 + lane;
-        slot[r] = i < n ? l1_digit(key[r], sp) : 0x10000u + lane;
-        peers[r] = __match_any_sync(0xffffffffu, slot[r]);
-    }
+        for (int r = 0; r < kSRounds; ++r) {
+            const int i = base + r * 32 + lane;
+            slot[r] = i < cnt ? l1_digit(kr[i], sp0) : 0x10000u + lane;
+            peers[r] = match_digit<11>(slot[r], nbits1, i < cnt);
+        }
 #pragma unroll
-    for (int r = 0; r < kG1Rounds; ++r) {
-        const uint32_t dg = slot[r];
-        const bool valid = dg < 0x10000u;
-        const uint32_t rank = __popc(peers[r] & lanemask_lt());
-        const uint32_t before = valid ? my[dg] : 0u;
-        __syncwarp();
-        if (valid && rank == 0) my[dg] = (uint16_t)(before + __popc(peers[r]));
-        __syncwarp();
-        slot[r] = (dg << 16) | (before + rank);
-    }
-    __syncthreads();
-    // per digit: exclusive over warps (in place), tile count; exclusive over digits -> loc
-    const int DPT = (nb1 + kG1Threads - 1) / kG1Threads;
-    uint32_t mysum = 0;
-    for (int j = 0; j < DPT; ++j) {
-        const int d = threadIdx.x * DPT + j;
-        if (d < nb1) {
-            uint32_t acc = 0;
+        for (int r = 0; r < kSRounds; ++r) {
+            const uint32_t dg = slot[r];
+            const bool valid = dg < 0x10000u;
+            const uint32_t rank = __popc(peers[r] & lanemask_lt());
+            const uint32_t before = valid ? my[dg] : 0u;
+            __syncwarp();
+            if (valid && rank == 0) my[dg] = (uint16_t)(before + __popc(peers[r]));
+            __syncwarp();
+            slot[r] = (dg << 16) | (before + rank);
+        }
+        __syncthreads();
+        // per digit: exclusive over warps (in place), tile count; exclusive over digits -> loc
+        const int DPT = (nb1 + kSThreads - 1) / kSThreads;
+        uint32_t mysum = 0;
+        for (int j = 0; j < DPT; ++j) {
+            const int d = threadIdx.x * DPT + j;
+            if (d < nb1) {
+                uint32_t acc = 0;
 #pragma unroll
-            for (int w = 0; w < kG1Warps; ++w) {
-                const uint32_t c = wrun[w * nb1 + d];
-                wrun[w * nb1 + d] = (uint16_t)acc;
-                acc += c;
+                for (int ww = 0; ww < kSWarps; ++ww) {
+                    const uint32_t c = wrun[ww * nb1 + d];
+                    wrun[ww * nb1 + d] = (uint16_t)acc;
+                    acc += c;
+                }
+                loc[d] = acc;
+                mysum += acc;
             }
-            loc[d] = acc;
-            mysum += acc;
         }
-    }
-    uint32_t ex = block_excl_scan<kG1Threads>(mysum, ws, nullptr);
-    for (int j = 0; j < DPT; ++j) {
-        const int d = threadIdx.x * DPT + j;
-        if (d < nb1) {
-            const uint32_t c = loc[d];
-            loc[d] = ex;
-            ex += c;
-            gpos[d] = binstart[(int64_t)t * (nb1 + 1) + d] + hist[((int64_t)t * T + tile) * nb1 + d];
+        uint32_t ex = block_excl_scan<kSThreads>(mysum, ws, nullptr);
+        for (int j = 0; j < DPT; ++j) {
+            const int d = threadIdx.x * DPT + j;
+            if (d < nb1) {
+                const uint32_t c = loc[d];
+                loc[d] = ex;
+                ex += c;
+                gpos[d] = binstart[(int64_t)t * (nb1 + 1) + d] + hist[((int64_t)t * T + tile) * nb1 + d];
+            }
         }
-    }
-    __syncthreads();
+        __syncthreads();
 #pragma unroll
-    for (int r = 0; r < kG1Rounds; ++r) {
-        const int64_t i = base + r * 32 + lane;
-        if (i < n) {
-            const uint32_t dg = slot[r] >> 16;
-            const uint32_t p = loc[dg] + wrun[warp * nb1 + dg] + (slot[r] & 0xffffu);
-            sk[p] = key[r];
-            sd[p] = (uint16_t)dg;
-            si[p] = IMPLICIT_IDS ? id_base + (uint32_t)i : iin[tb + i];
+        for (int r = 0; r < kSRounds; ++r) {
+            const int i = base + r * 32 + lane;
+            if (i < cnt) {
+                const uint32_t dg = slot[r] >> 16;
+                const uint32_t p = loc[dg] + wrun[warp * nb1 + dg] + (slot[r] & 0xffffu);
+                sp[p] = (uint16_t)i;
+                sd[p] = (uint16_t)dg;
+            }
         }
-    }
-    __syncthreads();
-    const int cnt = (int)min((int64_t)kG1Tile, n - (int64_t)tile * kG1Tile);
-    for (int p = threadIdx.x; p < cnt; p += kG1Threads) {
-        const uint64_t k = sk[p];
-        const uint32_t dg = sd[p];
-        const uint32_t pos = gpos[dg] + ((uint32_t)p - loc[dg]);
-        kout[tb + pos] = k;
-        iout[tb + pos] = si[p];
+        __syncthreads();
+        for (int p = threadIdx.x; p < cnt; p += kSThreads) {
+            const uint32_t i = sp[p], dg = sd[p];
+            const uint32_t pos = gpos[dg] + ((uint32_t)p - loc[dg]);
+            kout[tb + pos] = kr[i];
+            iout[tb + pos] = IMPLICIT_IDS ? id_base + (uint32_t)(tile * kG1Tile) + i : __ldg(ir + i);
+        }
     }
 }
 
@@ -490,7 +589,7 @@ __device__ void cta_digit_pass(const uint64_t* K, const PT* src, PT* dst, int64_
         const bool valid = i < a1;
         const uint32_t s = valid ? pget(src, i) : 0u;
         const uint32_t dg = valid ? df(K[s]) : 256u + lane;
-        const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+        const uint32_t peers = match_digit<8>(dg, 8, valid);
         if (valid && (peers & lanemask_lt()) == 0) my[dg] = (CT)(my[dg] + __popc(peers));
         __syncwarp();
     }
@@ -514,7 +613,7 @@ __device__ void cta_digit_pass(const uint64_t* K, const PT* src, PT* dst, int64_
         const bool valid = i < a1;
         const uint32_t s = valid ? pget(src, i) : 0u;
         const uint32_t dg = valid ? df(K[s]) : 256u + lane;
-        const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+        const uint32_t peers = match_digit<8>(dg, 8, valid);
         const uint32_t rank = __popc(peers & lanemask_lt());
         const uint32_t before = valid ? (uint32_t)my[dg] : 0u;
         __syncwarp();
@@ -714,32 +813,25 @@ __global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
             //     bits below sh if they vary there
             const uint16_t* src = pa;
             uint16_t* dst = pb;
+            // after the scatter, counter word w holds the END positions of digits 2w, 2w+1;
+            // a segment of equal key >> sh is exactly one digit bucket
+            auto digit_end = [&](uint32_t dg) { return (cnt[dg >> 1] >> ((dg & 1u) << 4)) & 0xffffu; };
             for (int r = threadIdx.x; r < len; r += kG2Threads) {
                 const uint32_t me = src[r];
                 const uint64_t kv = sk[me];
-                const uint64_t pr = kv >> sh;
-                const bool ep = r > 0 && (sk[src[r - 1]] >> sh) == pr;
-                const bool en = r + 1 < len && (sk[src[r + 1]] >> sh) == pr;
-                if (!ep && !en) {
+                const uint32_t dg = cd(kv);
+                const int e = (int)digit_end(dg);
+                const int h = dg ? (int)digit_end(dg - 1) : 0;
+                if (e - h == 1) {
                     dst[r] = (uint16_t)me;
                     continue;
                 }
-                int h = r;
-                while (h > 0 && r - h <= kG2Seg && (sk[src[h - 1]] >> sh) == pr) --h;
-                int e = r + 1;
-                while (e < len && e - h <= kG2Seg && (sk[src[e]] >> sh) == pr) ++e;
-                if (e - h > kG2Seg) {
-                    if (!ep) {  // head of a long segment: its end by binary search (prefixes ascend)
-                        int a0 = r + 1, b0 = (int)len;
-                        while (a0 < b0) {
-                            const int mid = (a0 + b0) >> 1;
-                            if ((sk[src[mid]] >> sh) == pr) a0 = mid + 1;
-                            else b0 = mid;
-                        }
+                if (e - h > kG2Seg) {   // long segment: position bitmap below
+                    if (r == h) {
                         const int slot = atomicAdd(&nlst, 1);
                         if (slot < kG2Long) {
-                            lst[2 * slot] = r;
-                            lst[2 * slot + 1] = a0;
+                            lst[2 * slot] = h;
+                            lst[2 * slot + 1] = e;
                         }
                     }
                     continue;
@@ -922,9 +1014,6 @@ __global__ void __launch_bounds__(kG2Threads) g3_rle(const uint64_t* __restrict_
     }
 }
 
-static size_t g1_scatter_smem(int nb1) {
-    return (size_t)kG1Tile * 14 + (size_t)nb1 * 8 + (size_t)kG1Warps * nb1 * 2;
-}
 static size_t g2_smem() { return (size_t)kG2Cap * 16 + (size_t)kG2Warps * 256 * 2; }
 
 size_t group_hist_words(int64_t n, int W) {
@@ -938,7 +1027,7 @@ size_t group_spec_bytes() { return sizeof(L1Spec); }
 // table by the digit of spec[0..L).
 static cudaError_t l1_pass(const uint64_t* kin, const uint32_t* iin, uint64_t* kout, uint32_t* iout, int64_t n, int L,
                            const L1Spec* spec, int nb1, uint32_t id_base, GroupScratch& sc, int span, int nchunks,
-                           uint32_t* chunkbin, cudaStream_t s) {
+                           uint32_t* chunkbin, int num_sms, cudaStream_t s) {
     const int T = (int)group_tiles(n);
     const dim3 g1(T, L);
     timing_begin("group_hist", s);
@@ -953,18 +1042,22 @@ static cudaError_t l1_pass(const uint64_t* kin, const uint32_t* iin, uint64_t* k
     count_launch();
     timing_end("group_scan", s);
     timing_begin("group_scatter", s);
-    const size_t sm1 = g1_scatter_smem(nb1);
+    const bool ids = iin != nullptr;
+    int nst = 2;
+    const size_t sm1 = g1_scatter_smem(nb1, ids, nst);
+    const int64_t items = (int64_t)T * L;
+    const int grid = (int)std::min<int64_t>(items, (int64_t)num_sms);
     cudaError_t e;
-    if (iin == nullptr) {
+    if (!ids) {
         e = cudaFuncSetAttribute(g1_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
         if (e != cudaSuccess) return e;
-        g1_scatter<true><<<g1, kG1Threads, sm1, s>>>(kin, nullptr, kout, iout, n, spec, nb1, sc.hist, sc.binstart, T,
-                                                     id_base);
+        g1_scatter<true><<<grid, kSThreads, sm1, s>>>(kin, nullptr, kout, iout, n, spec, nb1, sc.hist, sc.binstart, T,
+                                                      L, id_base, nst);
     } else {
         e = cudaFuncSetAttribute(g1_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
         if (e != cudaSuccess) return e;
-        g1_scatter<false><<<g1, kG1Threads, sm1, s>>>(kin, iin, kout, iout, n, spec, nb1, sc.hist, sc.binstart, T,
-                                                      id_base);
+        g1_scatter<false><<<grid, kSThreads, sm1, s>>>(kin, iin, kout, iout, n, spec, nb1, sc.hist, sc.binstart, T,
+                                                       L, id_base, nst);
     }
     count_launch();
     timing_end("group_scatter", s);
@@ -994,10 +1087,10 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
     timing_end("group_hist", s);
     if (lsd) {
         // narrow keys: full stable LSD sort on the varying bits (two passes), then RLE
-        e = l1_pass(keys, nullptr, sc.keys_a, sc.ids_a, n, L, spec, nb1, id_base, sc, 0, 0, nullptr, s);
+        e = l1_pass(keys, nullptr, sc.keys_a, sc.ids_a, n, L, spec, nb1, id_base, sc, 0, 0, nullptr, sc.num_sms, s);
         if (e != cudaSuccess) return e;
         uint64_t* kb = reinterpret_cast<uint64_t*>(sc.perm);
-        e = l1_pass(sc.keys_a, sc.ids_a, kb, out.ids, n, L, spec + L, nb1, id_base, sc, 0, 0, nullptr, s);
+        e = l1_pass(sc.keys_a, sc.ids_a, kb, out.ids, n, L, spec + L, nb1, id_base, sc, 0, 0, nullptr, sc.num_sms, s);
         if (e != cudaSuccess) return e;
         const int nch = (int)((n + kG2Cap - 1) / kG2Cap);
         timing_begin("group_sort", s);
@@ -1009,7 +1102,7 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
         return cudaGetLastError();
     }
     const int nch = group_chunks(n);
-    e = l1_pass(keys, nullptr, sc.keys_a, sc.ids_a, n, L, spec, nb1, id_base, sc, kG2Span, nch, sc.chunkbin, s);
+    e = l1_pass(keys, nullptr, sc.keys_a, sc.ids_a, n, L, spec, nb1, id_base, sc, kG2Span, nch, sc.chunkbin, sc.num_sms, s);
     if (e != cudaSuccess) return e;
     timing_begin("group_sort", s);
     e = cudaMemsetAsync(sc.state, 0, sizeof(unsigned long long) * (size_t)L * nch, s);

@@ -121,6 +121,7 @@ struct GroupScratch {
     unsigned long long* vmask;  // [L][2] OR of keys, OR of complemented keys
     void* spec;                 // [2][L] L1 digit specs (group.cu)
     uint32_t* chunkbin;         // [L][chunks+1] first L1 bin of every L2 chunk
+    int num_sms;
 };
 struct IndexDev {
     uint32_t* ids;    // [L][n]
