@@ -131,13 +131,13 @@ def peaks_tensor():
         return 1400.0, "fallback"
 
 
-def ncu_traffic(config, scheme):
-    """dram bytes per launch of the sketch kernel from the committed ncu summary."""
+def ncu_traffic(config, scheme, kernel="sketch"):
+    """dram bytes per launch of a kernel from the committed ncu summary (profiles/)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
             js = json.load(f)
-        ent = js.get(f"{config}/{scheme}/sketch")
+        ent = js.get(f"{config}/{scheme}/{kernel}")
         return ent.get("dram_bytes_per_launch") if ent else None
     except Exception:
         return None
@@ -275,7 +275,8 @@ def run_ours(args):
     kernel_ms = {k: pk.timing_get(k)[0] / max(1, args.steps) for k in
                  ("sketch", "sketch_query", "group_hist", "group_scan", "group_scatter", "group_sort", "lookup", "counts",
                   "global_offsets", "dense_gemm", "keys_from_proj")}
-    keep.clear()
+    idx_last = keep[-1] if keep else None
+    del keep[:-1]
     t = torch.tensor([ms_local], device=dev)
     if use_dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -340,6 +341,7 @@ def run_ours(args):
 
     hbm_peak, peak_kind = peaks()
     dense = scheme in ("E2LSH", "SRP")
+    kinfo = None
     if dense:
         # tensor-core dense baseline: algorithmic flops 2*n*m*d (the split into 3 bf16 terms
         # triples the executed MMA work; reported separately)
@@ -353,13 +355,37 @@ def run_ours(args):
                 "flops_per_launch": flops, "executed_mma_flops_per_launch": 3 * flops, "traffic": None,
                 "avg_launch_ms": avg}
     else:
-        bytes_per_point = 4 * cfg.d + 8 * cfg.L          # sketch kernel: read the point, write its L keys
-        sketch_avg_ms = sketch_ms / max(1, sketch_n)
-        achieved = bytes_per_point * n_local / (sketch_avg_ms * 1e-3) / 1e9 if sketch_avg_ms > 0 else None
-        roof = {"kernel": "sketch", "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "peak_kind": peak_kind,
-                "unit": "GB/s", "frac": (achieved / hbm_peak) if achieved else None,
-                "bytes_per_point": bytes_per_point, "traffic": ncu_traffic(cfg.name, scheme),
-                "avg_launch_ms": sketch_avg_ms}
+        # Algorithmic bytes per launch of each kernel of the step:
+        #   sketch        read the points (4d B) + write their L keys (8 B each)
+        #   group_hist    read the keys twice (varying-bit mask, L1 histogram)
+        #   group_scatter wide keys: read 8 B + write key+id 12 B per (table, point);
+        #                 narrow keys: two LSD passes (8 -> 12 B, then 12 -> 12 B)
+        #   group_sort    wide keys: read key+id 12 B, write id 4 B + (ukey, off) 12 B per bucket;
+        #                 narrow keys (RLE): read the sorted keys 8 B + 12 B per bucket
+        Ln = cfg.L * n_local
+        nb_total = sum(int(idx_last.view(t, copy=False)[1].numel()) for t in range(cfg.L)) if idx_last else Ln
+        narrow = (not h.e2lsh) and cfg.K <= 22
+        kbytes = {
+            "sketch": (4 * cfg.d + 8 * cfg.L) * n_local,
+            "group_hist": 16 * Ln,
+            "group_scatter": (20 + 24) * Ln if narrow else 20 * Ln,
+            "group_sort": (8 * Ln if narrow else 16 * Ln) + 12 * nb_total,
+        }
+        kinfo = {}
+        for k, b in kbytes.items():
+            tot_ms, cnt_l = pk.timing_get(k)
+            if cnt_l == 0:
+                continue
+            per_step_ms = tot_ms / max(1, args.steps)
+            gbs = b / (per_step_ms * 1e-3) / 1e9 if per_step_ms > 0 else None
+            kinfo[k] = {"ms_per_step": per_step_ms, "algorithmic_bytes": b, "achieved_gbs": gbs,
+                        "frac": (gbs / hbm_peak) if gbs else None}
+        dom = max(kinfo, key=lambda k: kinfo[k]["ms_per_step"])
+        roof = {"kernel": dom, "bound": "hbm", "achieved": kinfo[dom]["achieved_gbs"], "peak": hbm_peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": kinfo[dom]["frac"],
+                "algorithmic_bytes_per_launch": kinfo[dom]["algorithmic_bytes"],
+                "traffic": ncu_traffic(cfg.name, scheme, dom), "avg_launch_ms": kinfo[dom]["ms_per_step"],
+                "sketch_bytes_per_point": 4 * cfg.d + 8 * cfg.L}
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         rows = min(cfg.n, cpu_sample_rows(cfg))
@@ -375,6 +401,7 @@ def run_ours(args):
                    "K": cfg.K, "w": cfg.w, "queries_per_step": NQ, "parallelism": f"points sharded x{world}",
                    "l2": "inputs (%.2f GB) larger than L2; no flush" % (cfg.n * cfg.d * 4 / 1e9)},
         "roofline": roof,
+        "roofline_kernels": kinfo if not dense else None,
         "kernel_ms_per_step": kernel_ms,
         "cpu_baseline": cpu,
         "e2e": e2e,
