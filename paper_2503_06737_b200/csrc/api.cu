@@ -478,7 +478,6 @@ static lsh_status build_hcs_plan(lsh_handle* H) {
             ents.push_back(make_uint2(lists[g][i].first, y));
         }
     }
-    while (ents.size() % 4) ents.push_back(make_uint2(0u, HCS_EMPTY));   // pad to whole steps (no block)
     const size_t b_e = sizeof(uint2) * ents.size(), b_p = sizeof(uint16_t) * S, b_s = sizeof(uint32_t) * sgn.size(),
                  b_b = sizeof(uint16_t) * bp.size(), b_f = sizeof(int32_t) * bfirst.size(), b_w = wbins.size();
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };

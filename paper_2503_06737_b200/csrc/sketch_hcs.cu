@@ -50,39 +50,18 @@ __device__ __forceinline__ int32_t floor_code_h(float q, int* flags) {
     }
     return (int32_t)fq;
 }
-// a + sum of the C staged words listed at wo[0..C) (lane-relative base p)
-template <int C>
-__device__ __forceinline__ float sum_run(float a, const float* p, const uint16_t* wo) {
-    float b = 0.f;   // two chains for ILP
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-        if (c & 1) b += p[wo[c]];
-        else a += p[wo[c]];
-    }
-    return a + b;
-}
-// The count of a (warp, bin) pair is the same for every slab of the kernel, so this
-// switch always takes the same branch for a warp (no divergence, predictable).
+// a + sum of the cnt staged words listed at wo[0..cnt) (lane-relative base p); two
+// independent chains, the second half of each pair predicated
 __device__ __forceinline__ float sum_bin(float a, const float* p, const uint16_t* wo, uint32_t cnt) {
-    switch (cnt) {
-        case 0: return a;
-        case 1: return sum_run<1>(a, p, wo);
-        case 2: return sum_run<2>(a, p, wo);
-        case 3: return sum_run<3>(a, p, wo);
-        case 4: return sum_run<4>(a, p, wo);
-        case 5: return sum_run<5>(a, p, wo);
-        case 6: return sum_run<6>(a, p, wo);
-        case 7: return sum_run<7>(a, p, wo);
-        case 8: return sum_run<8>(a, p, wo);
-        case 9: return sum_run<9>(a, p, wo);
-        case 10: return sum_run<10>(a, p, wo);
-        case 11: return sum_run<11>(a, p, wo);
-        case 12: return sum_run<12>(a, p, wo);
-        default:
-            a = sum_run<12>(a, p, wo);
-            for (uint32_t c = 12; c < cnt; ++c) a += p[wo[c]];
-            return a;
+    float b = 0.f;
+    uint32_t c = 0;
+#pragma unroll 2
+    for (; c + 1 < cnt; c += 2) {
+        a += p[wo[c]];
+        b += p[wo[c + 1]];
     }
+    if (c < cnt) a += p[wo[c]];
+    return a + b;
 }
 __device__ __forceinline__ float4 ldg_stream_h(const float* p) {
     float4 r;
@@ -96,15 +75,36 @@ __device__ __forceinline__ float4 ldg_stream_h(const float* p) {
 // staged slab: word (k>>2)*129 + (k&3)*32 + r for coordinate k of row r (conflict-free
 // for the staging stores of lane = column threads and for the lane = row gathers)
 __host__ __device__ constexpr int hcs_tw(int S) { return (S / 4) * 129; }
-constexpr int kHcsStep = 4;   // slab entries per step (one batch of loads, two barriers)
-
+// shared memory: the staged block sum, the bin-sorted coordinate list, block codes
+// (double-buffered), b/w, entries
 size_t hcs_smem_bytes(int S, int M12, int m, int ne, int nst) {
     (void)nst;
-    return (size_t)kHcsStep * hcs_tw(S) * 4 + (size_t)S * 2 + (size_t)2 * M12 * 32 * 4 + (size_t)m * 4 +
-           (size_t)ne * 8 + 64;
+    return (size_t)hcs_tw(S) * 4 + (size_t)S * 2 + (size_t)2 * M12 * 32 * 4 + (size_t)m * 4 + (size_t)ne * 8 + 64;
 }
 
-// CPW = S / 16, BPW = M12 / 16 (bins per warp)
+namespace {
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+}  // namespace
+
+// CPW = S / 16, BPW = M12 / 16 (bins per warp).
+//
+// Block sums first: all slabs J of block g share the slab-internal map, so
+//   y_{g,b} = sum_J s(J) sum_{k in b} s12(k) x_J[k] = sum_{k in b} s12(k) Z_g[k],
+//   Z_g = sum_J s(J) x_J   (element-wise).
+// Z_g accumulates in registers (lane = column: one FFMA per input, no shared
+// memory); the slab map is applied once per block.  Each thread streams its own
+// 16-byte columns of every slab with 128-bit no-allocate loads into four rotating
+// register buffers (four slabs, 128 KB per SM, in flight), so the streaming loop
+// needs no block barrier; two barriers per block (stage Z_g transposed, then
+// gather bins / key the block's tables).
 template <int CPW, int BPW, bool E2>
 __global__ void __launch_bounds__(kThreads, 1)
     sketch_hcs_kernel(HcsPlanDev plan, DiscretizeDev dz, const float* __restrict__ X, int64_t n, int64_t ld,
@@ -115,28 +115,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int M12 = BPW * kWarps;
     constexpr int TW = hcs_tw(S);
     constexpr int Q4 = S / 4;              // float4 columns of a slab row
-    constexpr int RPI = kThreads / Q4;     // rows per load iteration
+    constexpr int RPI = kThreads / Q4;     // rows per thread step
     constexpr int VPT = 32 / RPI;          // float4 per thread per slab
-    constexpr int NB = kHcsStep * VPT;     // float4 per thread per step
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int m = plan.m, K = plan.K, ne = plan.nentries;   // ne: multiple of kHcsStep
-    float* T = reinterpret_cast<float*>(smem_raw);                            // [kHcsStep][TW]
-    uint16_t* wo = reinterpret_cast<uint16_t*>(T + kHcsStep * TW);            // [S]
+    const int m = plan.m, K = plan.K, ne = plan.nentries;
+    float* T = reinterpret_cast<float*>(smem_raw);                            // [TW]
+    uint16_t* wo = reinterpret_cast<uint16_t*>(T + TW);                       // [S]
     uint32_t* zs0 = reinterpret_cast<uint32_t*>(wo + S);                      // [2][M12][32]
     float* s_coff = reinterpret_cast<float*>(zs0 + 2 * M12 * 32);             // [m]
     uint2* ents = reinterpret_cast<uint2*>(s_coff + m);                       // [ne]
     const int64_t ntiles = (n + 31) >> 5;
-    int64_t tile = blockIdx.x;
-    if (tile >= ntiles) return;
+    if ((int64_t)blockIdx.x >= ntiles) return;
     for (int i = tid; i < m; i += kThreads) s_coff[i] = E2 ? __ldg(dz.c_off + i) : 0.f;
     for (int i = tid; i < ne; i += kThreads) ents[i] = __ldg(plan.entries + i);
     for (int i = tid; i < S; i += kThreads) wo[i] = __ldg(plan.pos + i);
     __syncthreads();
 
-    // staging column of this thread: coordinates 4*c4..4*c4+3 of rows r0 + v*RPI
     const int c4 = tid % Q4, r0 = tid / Q4;
     const uint32_t sg12 = (__ldg(plan.sgn + ((4 * c4) >> 5)) >> ((4 * c4) & 31)) & 0xfu;
-    // this warp's bins (balanced by coordinate count at plan time): id, start, count
+    const uint32_t sgm0 = (sg12 & 1u) << 31, sgm1 = ((sg12 >> 1) & 1u) << 31, sgm2 = ((sg12 >> 2) & 1u) << 31,
+                   sgm3 = ((sg12 >> 3) & 1u) << 31;
     uint32_t wb[BPW], bs[BPW], bc[BPW];
 #pragma unroll
     for (int j = 0; j < BPW; ++j) {
@@ -144,106 +142,121 @@ __global__ void __launch_bounds__(kThreads, 1)
         bs[j] = __ldg(plan.bp + wb[j]);
         bc[j] = __ldg(plan.bp + wb[j] + 1) - bs[j];
     }
-    int zpar = 0;
+    const int64_t vstride = (int64_t)RPI * ld;
 
-    float4 buf[NB];
-    auto load = [&](int64_t tl, int e0) {
-        const int64_t row0 = tl * 32 + r0;
+    // (tile, entry) cursors advanced incrementally (no 64-bit division per entry):
+    // `ct, ce` = entry being consumed, `lt, le` = entry being loaded (four ahead)
+    int64_t lt = blockIdx.x;
+    int le = 0;
+    auto load = [&](float4* buf) {   // loads entry (lt, le), then advances the cursor
+        if (lt < ntiles) {
+            const uint2 ent = ents[le];
+            if (!(ent.y & HCS_EMPTY)) {
+                const int64_t row0 = lt * 32 + r0;
+                const float* src = X + row0 * ld + (int64_t)ent.x * S + 4 * c4;
+                if (lt * 32 + 32 <= n) {
 #pragma unroll
-        for (int q = 0; q < kHcsStep; ++q) {
-            const uint2 ent = ents[e0 + q];
-            const float* src = X + row0 * ld + (int64_t)ent.x * S + 4 * c4;
-            const bool on = !(ent.y & HCS_EMPTY);
+                    for (int v = 0; v < VPT; ++v) buf[v] = ldg_stream_h(src + v * vstride);
+                } else {
 #pragma unroll
-            for (int v = 0; v < VPT; ++v)
-                buf[q * VPT + v] = (on && row0 + v * RPI < n) ? ldg_stream_h(src + (int64_t)v * RPI * ld)
-                                                              : make_float4(0.f, 0.f, 0.f, 0.f);
+                    for (int v = 0; v < VPT; ++v)
+                        buf[v] = row0 + v * RPI < n ? ldg_stream_h(src + v * vstride) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
+        }
+        if (++le == ne) {
+            le = 0;
+            lt += gridDim.x;
         }
     };
-    auto store = [&](int e0) {
+    float4 bA[VPT], bB[VPT], bC[VPT], bD[VPT];
+    load(bA);
+    load(bB);
+    load(bC);
+    load(bD);
+
+    float4 z[VPT];
 #pragma unroll
-        for (int q = 0; q < kHcsStep; ++q) {
-            const uint2 ent = ents[e0 + q];
-            const uint32_t sg = sg12 ^ ((ent.y & HCS_NEG) ? 0xfu : 0u);
-            float* dst = T + q * TW + c4 * 129 + r0;
+    for (int v = 0; v < VPT; ++v) z[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float cs = dz.c_scale;
+    int zpar = 0;
+    int64_t tile = blockIdx.x;
+    int ce = 0;
+    // one entry: fold its slab (from `buf`) into Z, refill `buf` with the entry four
+    // ahead, and after a block's last slab turn Z into the block's codes and keys
+    auto step = [&](float4* buf) -> bool {
+        if (tile >= ntiles) return true;
+        const uint2 ent = ents[ce];
+        if (!(ent.y & HCS_EMPTY)) {
+            const float sgn = (ent.y & HCS_NEG) ? -1.f : 1.f;
 #pragma unroll
             for (int v = 0; v < VPT; ++v) {
-                const float4 x = buf[q * VPT + v];
-                dst[v * RPI] = __uint_as_float(__float_as_uint(x.x) ^ ((sg & 1u) << 31));
-                dst[v * RPI + 32] = __uint_as_float(__float_as_uint(x.y) ^ (((sg >> 1) & 1u) << 31));
-                dst[v * RPI + 64] = __uint_as_float(__float_as_uint(x.z) ^ (((sg >> 2) & 1u) << 31));
-                dst[v * RPI + 96] = __uint_as_float(__float_as_uint(x.w) ^ (((sg >> 3) & 1u) << 31));
+                z[v].x = fmaf(sgn, buf[v].x, z[v].x);
+                z[v].y = fmaf(sgn, buf[v].y, z[v].y);
+                z[v].z = fmaf(sgn, buf[v].z, z[v].z);
+                z[v].w = fmaf(sgn, buf[v].w, z[v].w);
             }
         }
-    };
-
-    float acc[BPW];
-#pragma unroll
-    for (int j = 0; j < BPW; ++j) acc[j] = 0.f;
-    const float cs = dz.c_scale;
-    int e0 = 0;
-    load(tile, e0);
-    while (true) {
-        __syncthreads();  // previous gathers done with T
-        store(e0);
-        __syncthreads();
-        // next step's loads are in flight during the gathers below
-        int64_t ntile = tile;
-        int ne0 = e0 + kHcsStep;
-        if (ne0 == ne) {
-            ne0 = 0;
-            ntile += gridDim.x;
-        }
-        const bool has_next = ntile < ntiles;
-        if (has_next) load(ntile, ne0);
+        load(buf);
         const int64_t row = tile * 32 + lane;
-        const bool valid = row < n;
-#pragma unroll 1
-        for (int q = 0; q < kHcsStep; ++q) {
-            const uint2 ent = ents[e0 + q];
-            if (!(ent.y & HCS_EMPTY)) {
-                const float* p = T + q * TW + lane;
+        if (++ce == ne) {
+            ce = 0;
+            tile += gridDim.x;
+        }
+        if (!(ent.y & HCS_LAST)) return false;
+        // ---- block complete: stage Z_g (transposed, slab-internal sign applied) ----
+        {
+            float* dst = T + c4 * 129 + r0;
 #pragma unroll
-                for (int j = 0; j < BPW; ++j) acc[j] = sum_bin(acc[j], p, wo + bs[j], bc[j]);
-            }
-            if (ent.y & HCS_LAST) {
-                const int g = (int)(ent.y & HCS_BLOCK_MASK);
-                uint32_t* zs = zs0 + zpar * M12 * 32;   // double-buffered: no barrier after the keys
-                zpar ^= 1;
-#pragma unroll
-                for (int j = 0; j < BPW; ++j) {
-                    const int b = (int)wb[j];
-                    const int l = g * M12 + b;
-                    uint32_t z;
-                    if constexpr (E2) {
-                        z = (uint32_t)floor_code_h(fmaf(acc[j], cs, s_coff[l]), dz.flags);
-                        if (dbg && valid && out.codes) out.codes[row * m + l] = (int32_t)z;
-                    } else {
-                        z = acc[j] > 0.0f ? 1u : 0u;
-                        if (dbg && valid && out.bits && z)
-                            atomicOr(&out.bits[row * ((m + 31) >> 5) + (l >> 5)], 1u << (l & 31));
-                    }
-                    if (dbg && valid && out.proj) out.proj[row * m + l] = acc[j];
-                    zs[b * 32 + lane] = z;
-                    acc[j] = 0.f;
-                }
-                __syncthreads();
-                const int tpb = M12 / K;  // tables per block
-                if (tid < tpb * 32) {
-                    const int tb = tid >> 5;
-                    uint64_t fp = E2 ? LSHB_FNV_OFFSET : 0ull;
-                    for (int kk = 0; kk < K; ++kk) {
-                        const uint32_t z = zs[(tb * K + kk) * 32 + lane];
-                        if constexpr (E2) fp = (fp ^ (uint64_t)z) * LSHB_FNV_PRIME;
-                        else fp |= (uint64_t)z << kk;
-                    }
-                    if (valid && out.keys) out.keys[(int64_t)(g * tpb + tb) * n + row] = E2 ? fmix64_h(fp) : fp;
-                }
+            for (int v = 0; v < VPT; ++v) {
+                dst[v * RPI] = __uint_as_float(__float_as_uint(z[v].x) ^ sgm0);
+                dst[v * RPI + 32] = __uint_as_float(__float_as_uint(z[v].y) ^ sgm1);
+                dst[v * RPI + 64] = __uint_as_float(__float_as_uint(z[v].z) ^ sgm2);
+                dst[v * RPI + 96] = __uint_as_float(__float_as_uint(z[v].w) ^ sgm3);
+                z[v] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
         }
-        if (!has_next) break;
-        tile = ntile;
-        e0 = ne0;
+        __syncthreads();
+        const bool valid = row < n;
+        const int g = (int)(ent.y & HCS_BLOCK_MASK);
+        uint32_t* zs = zs0 + zpar * M12 * 32;   // double-buffered: no barrier after the keys
+        zpar ^= 1;
+        const float* p = T + lane;
+#pragma unroll
+        for (int j = 0; j < BPW; ++j) {
+            const float y = bc[j] ? sum_bin(0.f, p, wo + bs[j], bc[j]) : 0.f;
+            const int b = (int)wb[j];
+            const int l = g * M12 + b;
+            uint32_t zc;
+            if constexpr (E2) {
+                zc = (uint32_t)floor_code_h(fmaf(y, cs, s_coff[l]), dz.flags);
+                if (dbg && valid && out.codes) out.codes[row * m + l] = (int32_t)zc;
+            } else {
+                zc = y > 0.0f ? 1u : 0u;
+                if (dbg && valid && out.bits && zc) atomicOr(&out.bits[row * ((m + 31) >> 5) + (l >> 5)], 1u << (l & 31));
+            }
+            if (dbg && valid && out.proj) out.proj[row * m + l] = y;
+            zs[b * 32 + lane] = zc;
+        }
+        __syncthreads();   // codes complete; every gather is done with T
+        const int tpb = M12 / K;  // tables per block
+        if (tid < tpb * 32) {
+            const int tb = tid >> 5;
+            uint64_t fp = E2 ? LSHB_FNV_OFFSET : 0ull;
+            for (int kk = 0; kk < K; ++kk) {
+                const uint32_t zc = zs[(tb * K + kk) * 32 + lane];
+                if constexpr (E2) fp = (fp ^ (uint64_t)zc) * LSHB_FNV_PRIME;
+                else fp |= (uint64_t)zc << kk;
+            }
+            if (valid && out.keys) out.keys[(int64_t)(g * tpb + tb) * n + row] = E2 ? fmix64_h(fp) : fp;
+        }
+        return false;
+    };
+    while (true) {
+        if (step(bA)) break;
+        if (step(bB)) break;
+        if (step(bC)) break;
+        if (step(bD)) break;
     }
 }
 
