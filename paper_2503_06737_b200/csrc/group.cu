@@ -359,34 +359,49 @@ __global__ void __launch_bounds__(kSThreads, 1)
         const uint64_t a = reinterpret_cast<uint64_t>(kin + (int64_t)t * n + (int64_t)tile * kG1Tile);
         return cnt == kG1Tile && (a & 15) == 0;
     };
-    auto issue = [&](int64_t it) {  // thread 0
-        const int64_t w = (int64_t)blockIdx.x + it * gridDim.x;
-        if (w >= items) return;
-        const int st = (int)(it % nst);
-        const int t = (int)(w / T), tile = (int)(w % T);
-        if (!bulk_ok(t, tile)) {
-            g_mbar_arrive_tx(bars + st, 0u);
-            return;
+    // work-item cursors advanced incrementally (no 64-bit division per item):
+    // item w = blockIdx.x + it * grid  ->  (table t, tile), t-major
+    struct Cur {
+        int t, tile;
+    };
+    auto advance = [&](Cur& c) {
+        c.tile += gridDim.x;
+        while (c.tile >= T) {
+            c.tile -= T;
+            ++c.t;
         }
-        const int64_t off = (int64_t)t * n + (int64_t)tile * kG1Tile;
-        g_mbar_arrive_tx(bars + st, kG1Tile * 8u);
-        g_bulk(rk + (size_t)st * kG1Tile, kin + off, kG1Tile * 8u, bars + st);
+    };
+    Cur ci{(int)(blockIdx.x / T), (int)(blockIdx.x % T)};   // next item to issue (thread 0)
+    int ist = 0;
+    auto issue = [&]() {  // thread 0: bulk copy of item ci into stage ist, then advance
+        if (ci.t < L) {
+            if (!bulk_ok(ci.t, ci.tile)) {
+                g_mbar_arrive_tx(bars + ist, 0u);
+            } else {
+                const int64_t off = (int64_t)ci.t * n + (int64_t)ci.tile * kG1Tile;
+                g_mbar_arrive_tx(bars + ist, kG1Tile * 8u);
+                g_bulk(rk + (size_t)ist * kG1Tile, kin + off, kG1Tile * 8u, bars + ist);
+            }
+        }
+        advance(ci);
+        if (++ist == nst) ist = 0;
     };
     if (threadIdx.x == 0)
-        for (int i = 0; i < nst - 1; ++i) issue(i);
+        for (int i = 0; i < nst - 1; ++i) issue();
 
-    for (int64_t it = 0;; ++it) {
-        const int64_t w = (int64_t)blockIdx.x + it * gridDim.x;
-        if (w >= items) break;
-        const int st = (int)(it % nst);
-        const int t = (int)(w / T), tile = (int)(w % T);
+    Cur cc{(int)(blockIdx.x / T), (int)(blockIdx.x % T)};   // item being processed
+    int st = 0;
+    uint32_t phase = 0;
+    for (;; advance(cc)) {
+        if (cc.t >= L) break;
+        const int t = cc.t, tile = cc.tile;
         const L1Spec sp0 = spec[t];
         const int nbits1 = sp0.nbits;
         const int64_t tb = (int64_t)t * n;
         const int cnt = (int)min((int64_t)kG1Tile, n - (int64_t)tile * kG1Tile);
         uint64_t* kr = rk + (size_t)st * kG1Tile;
         const uint32_t* ir = IMPLICIT_IDS ? nullptr : iin + tb + (int64_t)tile * kG1Tile;
-        g_mbar_wait(bars + st, (uint32_t)((it / nst) & 1));
+        g_mbar_wait(bars + st, phase);
         for (int i = threadIdx.x; i < kSWarps * nb1; i += kSThreads) wrun[i] = 0;
         if (!bulk_ok(t, tile)) {
             for (int i = threadIdx.x; i < cnt; i += kSThreads) kr[i] = kin[tb + (int64_t)tile * kG1Tile + i];
@@ -394,7 +409,11 @@ __global__ void __launch_bounds__(kSThreads, 1)
         __syncthreads();   // tile in smem; previous write-out finished with its stage
         if (threadIdx.x == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(it + nst - 1);   // into the stage the previous item used
+            issue();   // into the stage the previous item used
+        }
+        if (++st == nst) {
+            st = 0;
+            phase ^= 1u;
         }
         uint16_t* my = wrun + warp * nb1;
         uint32_t slot[kSRounds], peers[kSRounds];
