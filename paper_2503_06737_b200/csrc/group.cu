@@ -762,18 +762,15 @@ __global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
         uint16_t* pa = reinterpret_cast<uint16_t*>(g2_dsm + kG2Cap * 12);     // [cap]
         uint16_t* pb = pa + kG2Cap;                                           // [cap]
         uint32_t* cnt = reinterpret_cast<uint32_t*>(pb + kG2Cap);             // [2048] two u16 counters per word
-        uint64_t o = 0, an = ~0ull;
         for (int i = threadIdx.x; i < len; i += kG2Threads) {
-            const uint64_t k = gk[i];
-            sk[i] = k;
+            sk[i] = gk[i];
             si[i] = gi[i];
-            o |= k;
-            an &= k;
         }
         __syncthreads();
-        // bits that still vary inside the L1 bins (the bins of the chunk are in order)
-        const uint64_t varying = cta_varying_from(o, an, red) & (len > 0 ? sp.below : 0ull);
-        const int hb = varying ? 64 - __clzll((long long)varying) : 0;
+        // the bits below the L1 digit (the table's varying-bit mask chooses the window;
+        // a chunk whose keys are constant there still sorts correctly, through the
+        // long-segment path)
+        const int hb = (sp.nbits == 0 || len == 0) ? 0 : 64 - __clzll((long long)sp.below);
         const int G = bin_hi - bin_lo;
         const int gb = G > 1 ? 32 - __clz(G - 1) : 0;    // bits of the bin index inside the chunk
         uint16_t* cur = nullptr;
