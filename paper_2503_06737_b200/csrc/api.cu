@@ -531,24 +531,25 @@ static lsh_status build_plan(lsh_handle* H) {
     }
     const uint32_t ZW = (uint32_t)(Q / 4) * 129u;
     int max_cnt = 0;
-    std::vector<uint32_t> pairs(m), bigmask(p->L, 0);
+    std::vector<uint32_t> pairs(2 * (size_t)m), bigmask(p->L, 0);
     for (int l = 0; l < m; ++l) {
         const uint32_t c = bin_ptr[l + 1] - bin_ptr[l];
         max_cnt = std::max(max_cnt, (int)c);
         const uint32_t a = c >= 1 ? ent[bin_ptr[l]] : ZW;
         const uint32_t b = c >= 2 ? ent[bin_ptr[l] + 1] : ZW;
-        pairs[l] = a | (b << 16);
+        pairs[2 * l] = a * 4u;       // byte offsets inside the staged tile
+        pairs[2 * l + 1] = b * 4u;
         if (c > 2 && p->K <= 32) bigmask[l / p->K] |= 1u << (l % p->K);
     }
     CK(cudaMalloc(&H->d_entries, sizeof(uint16_t) * std::max(1, d)));
     CK(cudaMalloc(&H->d_binptr, sizeof(uint32_t) * bin_ptr.size()));
     CK(cudaMalloc(&H->d_signs, sizeof(uint32_t) * sign_bits.size()));
-    CK(cudaMalloc(&H->d_pairs, sizeof(uint32_t) * m));
+    CK(cudaMalloc(&H->d_pairs, sizeof(uint32_t) * 2 * (size_t)m));
     CK(cudaMalloc(&H->d_bigmask, sizeof(uint32_t) * p->L));
     CK(cudaMemcpy(H->d_entries, ent.data(), sizeof(uint16_t) * d, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(H->d_binptr, bin_ptr.data(), sizeof(uint32_t) * bin_ptr.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(H->d_signs, sign_bits.data(), sizeof(uint32_t) * sign_bits.size(), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(H->d_pairs, pairs.data(), sizeof(uint32_t) * m, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(H->d_pairs, pairs.data(), sizeof(uint32_t) * 2 * (size_t)m, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(H->d_bigmask, bigmask.data(), sizeof(uint32_t) * p->L, cudaMemcpyHostToDevice));
     H->plan = SketchPlanDev{d, m, p->L, p->K, Q, vpt, 1, max_cnt, H->d_entries, H->d_binptr, H->d_signs,
                             H->d_pairs, H->d_bigmask};

@@ -27,7 +27,7 @@ struct SketchPlanDev {
     const uint16_t* pos;        // [d] staged-tile word offset of the coordinate at each bin-sorted index
     const uint32_t* bin_ptr;    // [nchunks][m+1] absolute index (chunk start + rank) where each bin starts
     const uint32_t* sign_bits;  // [ceil(d/32)] bit j set = sign(j) = -1 (applied while staging)
-    const uint32_t* pairs;      // [m] per bin: word offsets (pos*33) of its first two staged coordinates,
+    const uint32_t* pairs;      // [2m] per bin: byte offsets (in the staged tile) of its first two coordinates,
                                 //     lo 16 bits / hi 16 bits; missing ones point at the zero slot Q
     const uint32_t* bigmask;    // [L] bit k set: bin k of table t has more than 2 coordinates
 };

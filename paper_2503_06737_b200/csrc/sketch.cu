@@ -126,7 +126,7 @@ struct KeyAcc {
 //   ent  [d]   u16              T word offset of the coordinate at each bin-sorted index
 //   coff [m]   fp32             b_l / w
 //   sgn  [ceil(d/32)] u32       bit j set: sign(j) = -1
-//   pairs[m]   u32              word offsets of each bin's first two coordinates (ZW if missing)
+//   pairs[2m]  u32              byte offsets of each bin's first two coordinates (zero slot if missing)
 //   big  [L]   u32              bit k: bin k of table t has more than two coordinates
 struct SketchSmem {
     size_t t, bp, cnt, ent, coff, sgn, pairs, big, total;
@@ -138,7 +138,7 @@ __host__ __device__ inline SketchSmem sketch_smem_layout(int Q, int m, int d, in
     x += ((size_t)(Q / 4) * 129 + 64) * 4;
     x = (x + 15) / 16 * 16;
     o.pairs = x;
-    x += (size_t)m * 4;
+    x += (size_t)m * 8;
     x = (x + 15) / 16 * 16;
     o.coff = x;
     x += (size_t)m * 4;
@@ -196,7 +196,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t cn = __ldg(plan.bin_ptr + i + 1) - __ldg(plan.bin_ptr + i);
         s_cnt[i] = (uint8_t)(cn < 255u ? cn : 255u);
         s_coff[i] = E2 ? __ldg(dz.c_off + i) : 0.f;
-        s_pairs[i] = __ldg(plan.pairs + i);
+        s_pairs[2 * i] = __ldg(plan.pairs + 2 * i);
+        s_pairs[2 * i + 1] = __ldg(plan.pairs + 2 * i + 1);
     }
     for (int i = tid; i < d; i += kThreads) s_ent[i] = __ldg(plan.pos + i);
     for (int i = tid; i < (d + 31) / 32; i += kThreads) s_sgn[i] = __ldg(plan.sign_bits + i);
@@ -292,22 +293,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (KT > 0) {
             // hot path: each bin's first two coordinates through `pairs` (branch-free; a
             // missing one reads the zero slot), rare fix-ups for fuller bins, then
-            // discretise + key for the K bins of the table.
+            // discretise + key for the K bins of the table.  Two tables per iteration: their
+            // fingerprint chains (16 dependent multiply steps each) interleave.
+#pragma unroll 2
             for (int t = warp; t < L; t += kWarps) {
                 float acc[KT];
                 {
-                    uint32_t pw[KT];
-                    const uint4* pp4 = reinterpret_cast<const uint4*>(s_pairs + t * KT);
+                    // two byte offsets per bin, read 2 bins per 128-bit load; one add each
+                    const uint4* pp4 = reinterpret_cast<const uint4*>(s_pairs + t * KT * 2);
+                    const char* Tb = reinterpret_cast<const char*>(Tl);
 #pragma unroll
-                    for (int i = 0; i < KT / 4; ++i) {
+                    for (int i = 0; i < KT / 2; ++i) {
                         const uint4 v = pp4[i];
-                        pw[4 * i] = v.x;
-                        pw[4 * i + 1] = v.y;
-                        pw[4 * i + 2] = v.z;
-                        pw[4 * i + 3] = v.w;
+                        acc[2 * i] = *reinterpret_cast<const float*>(Tb + v.x) + *reinterpret_cast<const float*>(Tb + v.y);
+                        acc[2 * i + 1] =
+                            *reinterpret_cast<const float*>(Tb + v.z) + *reinterpret_cast<const float*>(Tb + v.w);
                     }
-#pragma unroll
-                    for (int kk = 0; kk < KT; ++kk) acc[kk] = Tl[pw[kk] & 0xffffu] + Tl[pw[kk] >> 16];
                 }
                 const uint32_t big = s_big[t];
                 if (big) {
