@@ -195,16 +195,31 @@ __global__ void g0_spec(const unsigned long long* __restrict__ vm, int L, int B1
 // ---------------------------------------------------------------------------
 // L1: histogram, per-bin tile scan, bin starts, stable scatter
 // ---------------------------------------------------------------------------
+// mode 0: digit = spec's digit.  mode 1 (wide keys, speculative): digit = the top
+// b1 bits of the W-bit key, and the key OR / complement-OR per table are
+// accumulated for the varying-bit mask in the same read.  mode 2: redo mode 1's
+// histogram with the spec digit, only for tables whose varying top bits are not the
+// top b1 bits (other CTAs exit at once).
 __global__ void __launch_bounds__(kG1Threads) g1_hist(const uint64_t* __restrict__ keys, int64_t n,
                                                     const L1Spec* __restrict__ spec, int nb1,
-                                                    uint32_t* __restrict__ hist, int T) {
+                                                    uint32_t* __restrict__ hist, int T, int mode, int W, int b1,
+                                                    unsigned long long* __restrict__ vm) {
     extern __shared__ uint32_t g1_cnt[];
     const int t = blockIdx.y, tile = blockIdx.x;
+    L1Spec sp;
+    if (mode == 1) {
+        sp.nbits = b1;
+        sp.shift = W - b1;
+        sp.below = 0;
+    } else {
+        sp = spec[t];
+        if (mode == 2 && sp.nbits == b1 && sp.shift == W - b1) return;
+    }
+    uint64_t o = 0, no = 0;
     for (int i = threadIdx.x; i < nb1; i += kG1Threads) g1_cnt[i] = 0;
     const int64_t t0 = (int64_t)tile * kG1Tile;
     const uint64_t* kt = keys + (int64_t)t * n + t0;
     const int cn = (int)min((int64_t)kG1Tile, n - t0);
-    const L1Spec sp = spec[t];
     constexpr int R = 16;   // keys per thread per batch
 #pragma unroll 1
     for (int b0 = 0; b0 < kG1Tile; b0 += R * kG1Threads) {
@@ -218,7 +233,24 @@ __global__ void __launch_bounds__(kG1Threads) g1_hist(const uint64_t* __restrict
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int i = b0 + r * kG1Threads + threadIdx.x;
-            if (i < cn) atomicAdd(&g1_cnt[l1_digit(k[r], sp)], 1u);
+            if (i < cn) {
+                atomicAdd(&g1_cnt[l1_digit(k[r], sp)], 1u);
+                if (mode == 1) {
+                    o |= k[r];
+                    no |= ~k[r];
+                }
+            }
+        }
+    }
+    if (mode == 1) {
+#pragma unroll
+        for (int sft = 16; sft > 0; sft >>= 1) {
+            o |= __shfl_xor_sync(0xffffffffu, o, sft);
+            no |= __shfl_xor_sync(0xffffffffu, no, sft);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicOr(vm + 2 * t, (unsigned long long)o);
+            atomicOr(vm + 2 * t + 1, (unsigned long long)no);
         }
     }
     __syncthreads();
@@ -1043,13 +1075,15 @@ size_t group_spec_bytes() { return sizeof(L1Spec); }
 // table by the digit of spec[0..L).
 static cudaError_t l1_pass(const uint64_t* kin, const uint32_t* iin, uint64_t* kout, uint32_t* iout, int64_t n, int L,
                            const L1Spec* spec, int nb1, uint32_t id_base, GroupScratch& sc, int span, int nchunks,
-                           uint32_t* chunkbin, int num_sms, cudaStream_t s) {
+                           uint32_t* chunkbin, int num_sms, cudaStream_t s, bool hist_done = false) {
     const int T = (int)group_tiles(n);
     const dim3 g1(T, L);
-    timing_begin("group_hist", s);
-    g1_hist<<<g1, kG1Threads, nb1 * sizeof(uint32_t), s>>>(kin, n, spec, nb1, sc.hist, T);
-    count_launch();
-    timing_end("group_hist", s);
+    if (!hist_done) {
+        timing_begin("group_hist", s);
+        g1_hist<<<g1, kG1Threads, nb1 * sizeof(uint32_t), s>>>(kin, n, spec, nb1, sc.hist, T, 0, 64, 0, nullptr);
+        count_launch();
+        timing_end("group_hist", s);
+    }
     timing_begin("group_scan", s);
     const int64_t warps = (int64_t)L * ((nb1 + 31) / 32);
     g1_scan<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(sc.hist, T, L, nb1, sc.tot);
@@ -1096,10 +1130,24 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
     timing_begin("group_hist", s);
     e = cudaMemsetAsync(sc.vmask, 0, sizeof(unsigned long long) * 2 * L, s);
     if (e != cudaSuccess) return e;
-    g0_mask<<<dim3((unsigned)((n + 8191) / 8192), L), 256, 0, s>>>(keys, n, sc.vmask);
-    count_launch();
-    g0_spec<<<(L + 127) / 128, 128, 0, s>>>(sc.vmask, L, B1, lsd ? 2 : 1, spec);
-    count_launch();
+    const int T = (int)group_tiles(n);
+    if (!lsd) {
+        // wide keys: one read of the keys gives the top-B1-bit histograms AND the
+        // varying mask; tables whose top B1 bits do not all vary are re-histogrammed
+        g1_hist<<<dim3(T, L), kG1Threads, nb1 * sizeof(uint32_t), s>>>(keys, n, spec, nb1, sc.hist, T, 1, W, B1,
+                                                                      sc.vmask);
+        count_launch();
+        g0_spec<<<(L + 127) / 128, 128, 0, s>>>(sc.vmask, L, B1, 1, spec);
+        count_launch();
+        g1_hist<<<dim3(T, L), kG1Threads, nb1 * sizeof(uint32_t), s>>>(keys, n, spec, nb1, sc.hist, T, 2, W, B1,
+                                                                      nullptr);
+        count_launch();
+    } else {
+        g0_mask<<<dim3((unsigned)((n + 8191) / 8192), L), 256, 0, s>>>(keys, n, sc.vmask);
+        count_launch();
+        g0_spec<<<(L + 127) / 128, 128, 0, s>>>(sc.vmask, L, B1, 2, spec);
+        count_launch();
+    }
     timing_end("group_hist", s);
     if (lsd) {
         // narrow keys: full stable LSD sort on the varying bits (two passes), then RLE
@@ -1118,7 +1166,8 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
         return cudaGetLastError();
     }
     const int nch = group_chunks(n);
-    e = l1_pass(keys, nullptr, sc.keys_a, sc.ids_a, n, L, spec, nb1, id_base, sc, kG2Span, nch, sc.chunkbin, sc.num_sms, s);
+    e = l1_pass(keys, nullptr, sc.keys_a, sc.ids_a, n, L, spec, nb1, id_base, sc, kG2Span, nch, sc.chunkbin, sc.num_sms, s,
+                true);
     if (e != cudaSuccess) return e;
     timing_begin("group_sort", s);
     e = cudaMemsetAsync(sc.state, 0, sizeof(unsigned long long) * (size_t)L * nch, s);
