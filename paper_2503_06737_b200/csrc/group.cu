@@ -362,7 +362,11 @@ size_t g1_scatter_smem(int nb1, bool ids, int nst) {
     return 64 + (size_t)nst * kG1Tile * 8 + (size_t)kG1Tile * 4 + (size_t)nb1 * 8 + (size_t)kSWarps * nb1 * 2;
 }
 
-template <bool IMPLICIT_IDS>
+// STABLE = false (wide-key MSD pass): ranks inside a digit come from one shared
+// atomicAdd per key (order inside a tile's run of a digit is then arbitrary; the
+// per-chunk sort orders ties by id).  STABLE = true (narrow-key LSD passes, which
+// need stability): warp-private counts + ballot digit match.
+template <bool IMPLICIT_IDS, bool STABLE>
 __global__ void __launch_bounds__(kSThreads, 1)
     g1_scatter(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ iin, uint64_t* __restrict__ kout,
                uint32_t* __restrict__ iout, int64_t n, const L1Spec* __restrict__ spec, int nb1,
@@ -447,25 +451,38 @@ __global__ void __launch_bounds__(kSThreads, 1)
             st = 0;
             phase ^= 1u;
         }
-        uint16_t* my = wrun + warp * nb1;
-        uint32_t slot[kSRounds], peers[kSRounds];
+        uint32_t slot[kSRounds];
         const int base = warp * (kG1Tile / kSWarps);
+        if constexpr (STABLE) {
+            uint16_t* my = wrun + warp * nb1;
+            uint32_t peers[kSRounds];
 #pragma unroll
-        for (int r = 0; r < kSRounds; ++r) {
-            const int i = base + r * 32 + lane;
-            slot[r] = i < cnt ? l1_digit(kr[i], sp0) : 0x10000u + lane;
-            peers[r] = match_digit<11>(slot[r], nbits1, i < cnt);
-        }
+            for (int r = 0; r < kSRounds; ++r) {
+                const int i = base + r * 32 + lane;
+                slot[r] = i < cnt ? l1_digit(kr[i], sp0) : 0x10000u + lane;
+                peers[r] = match_digit<11>(slot[r], nbits1, i < cnt);
+            }
 #pragma unroll
-        for (int r = 0; r < kSRounds; ++r) {
-            const uint32_t dg = slot[r];
-            const bool valid = dg < 0x10000u;
-            const uint32_t rank = __popc(peers[r] & lanemask_lt());
-            const uint32_t before = valid ? my[dg] : 0u;
-            __syncwarp();
-            if (valid && rank == 0) my[dg] = (uint16_t)(before + __popc(peers[r]));
-            __syncwarp();
-            slot[r] = (dg << 16) | (before + rank);
+            for (int r = 0; r < kSRounds; ++r) {
+                const uint32_t dg = slot[r];
+                const bool valid = dg < 0x10000u;
+                const uint32_t rank = __popc(peers[r] & lanemask_lt());
+                const uint32_t before = valid ? my[dg] : 0u;
+                __syncwarp();
+                if (valid && rank == 0) my[dg] = (uint16_t)(before + __popc(peers[r]));
+                __syncwarp();
+                slot[r] = (dg << 16) | (before + rank);
+            }
+        } else {
+            uint32_t* c32 = reinterpret_cast<uint32_t*>(wrun);   // [nb1] tile counts
+#pragma unroll
+            for (int r = 0; r < kSRounds; ++r) {
+                const int i = base + r * 32 + lane;
+                if (i < cnt) {
+                    const uint32_t dg = l1_digit(kr[i], sp0);
+                    slot[r] = (dg << 16) | atomicAdd(&c32[dg], 1u);
+                }
+            }
         }
         __syncthreads();
         // per digit: exclusive over warps (in place), tile count; exclusive over digits -> loc
@@ -475,11 +492,15 @@ __global__ void __launch_bounds__(kSThreads, 1)
             const int d = threadIdx.x * DPT + j;
             if (d < nb1) {
                 uint32_t acc = 0;
+                if constexpr (STABLE) {
 #pragma unroll
-                for (int ww = 0; ww < kSWarps; ++ww) {
-                    const uint32_t c = wrun[ww * nb1 + d];
-                    wrun[ww * nb1 + d] = (uint16_t)acc;
-                    acc += c;
+                    for (int ww = 0; ww < kSWarps; ++ww) {
+                        const uint32_t c = wrun[ww * nb1 + d];
+                        wrun[ww * nb1 + d] = (uint16_t)acc;
+                        acc += c;
+                    }
+                } else {
+                    acc = reinterpret_cast<const uint32_t*>(wrun)[d];
                 }
                 loc[d] = acc;
                 mysum += acc;
@@ -501,7 +522,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
             const int i = base + r * 32 + lane;
             if (i < cnt) {
                 const uint32_t dg = slot[r] >> 16;
-                const uint32_t p = loc[dg] + wrun[warp * nb1 + dg] + (slot[r] & 0xffffu);
+                const uint32_t p = loc[dg] + (STABLE ? (uint32_t)wrun[warp * nb1 + dg] : 0u) + (slot[r] & 0xffffu);
                 sp[p] = (uint16_t)i;
                 sd[p] = (uint16_t)dg;
             }
@@ -528,6 +549,7 @@ struct G2Args {
     const L1Spec* spec;         // [L]
     int64_t n;
     int nb1;
+    uint32_t id_base;           // ids of a table are id_base + row
     int nchunks;                // L2 chunks per table
     const uint32_t* chunkbin;   // [L][nchunks+1] first L1 bin of every chunk
     IndexDev out;
@@ -582,7 +604,8 @@ __device__ uint32_t chained_prefix_warp(unsigned long long* st, int b, uint32_t 
 }
 
 // Bits that vary over K[0..len) (OR ^ AND).
-__device__ uint64_t cta_varying(const uint64_t* K, int64_t len, unsigned long long* red) {
+template <typename KE>
+__device__ uint64_t cta_varying(const KE* K, int64_t len, unsigned long long* red) {
     if (threadIdx.x == 0) {
         red[0] = 0ull;
         red[1] = ~0ull;
@@ -626,8 +649,8 @@ struct ChunkDigit {
     }
 };
 
-template <typename PT, typename CT, typename DF = ShiftDigit>
-__device__ void cta_digit_pass(const uint64_t* K, const PT* src, PT* dst, int64_t len, DF df, CT* wcnt,
+template <typename PT, typename CT, typename DF = ShiftDigit, typename KE = uint64_t>
+__device__ void cta_digit_pass(const KE* K, const PT* src, PT* dst, int64_t len, DF df, CT* wcnt,
                                uint32_t* ws) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t per = ((len + kG2Warps - 1) / kG2Warps + 31) / 32 * 32;
@@ -680,14 +703,14 @@ __device__ void cta_digit_pass(const uint64_t* K, const PT* src, PT* dst, int64_
 // LSD passes over the 8-bit digits below `top` that vary (bit set in `varying`);
 // the permutation starts in *cur (nullptr = identity) and ends in *cur.  Both
 // ping-pong buffers are [len].
-template <typename PT, typename CT>
-__device__ void cta_lsd(const uint64_t* K, PT*& cur, PT* b0, PT* b1, int64_t len, int top, uint64_t varying, CT* wcnt,
+template <typename PT, typename CT, typename KE = uint64_t>
+__device__ void cta_lsd(const KE* K, PT*& cur, PT* b0, PT* b1, int64_t len, int top, uint64_t varying, CT* wcnt,
                         uint32_t* ws) {
     for (int sh = 0; sh < top; sh += 8) {
         const uint64_t dmask = (top - sh >= 8 ? 0xffull : ((1ull << (top - sh)) - 1)) << sh;
         if ((varying & dmask) == 0) continue;
         PT* dst = (cur == b0) ? b1 : b0;
-        cta_digit_pass<PT, CT>(K, cur, dst, len, ShiftDigit{sh}, wcnt, ws);
+        cta_digit_pass<PT, CT, ShiftDigit, KE>(K, cur, dst, len, ShiftDigit{sh}, wcnt, ws);
         cur = dst;
     }
 }
@@ -742,6 +765,7 @@ __device__ void cta_emit(const uint64_t* K, const uint32_t* ID, const PT* perm, 
 
 // OR / AND of per-thread key aggregates over the block (red pre-initialised to {0, ~0}).
 __device__ __forceinline__ uint64_t cta_varying_from(uint64_t o, uint64_t an, unsigned long long* red) {
+    __syncthreads();   // a previous call's reset of red is visible
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) {
         o |= __shfl_xor_sync(0xffffffffu, o, s);
@@ -759,6 +783,54 @@ __device__ __forceinline__ uint64_t cta_varying_from(uint64_t o, uint64_t an, un
         red[1] = ~0ull;
     }
     return v;
+}
+
+// Order a permutation range by id when its items are in L1 order: the wide-key L1
+// pass writes each tile's items of a bin as one run, bins in order and tiles in
+// order inside a bin, ids shuffled inside a run.  Along any stable sub-range the run
+// id (L1 bin, tile) is non-decreasing; every maximal run is sorted by the low 13 id
+// bits with an 8192-bit bitmap.  src -> dst (both [len], global).
+__device__ void cta_sort_tile_runs(const uint32_t* ID, const uint64_t* K, const L1Spec& sp, const uint32_t* src,
+                                   uint32_t* dst, int64_t len, uint32_t id_base, uint32_t* bm /*[256]*/,
+                                   uint16_t* loc /*[8192]*/, uint32_t* ws) {
+    auto run_of = [&](int64_t r) {
+        const uint32_t p = pget(src, r);
+        return ((uint64_t)l1_digit(K[p], sp) << 32) | ((ID[p] - id_base) >> 13);
+    };
+    int64_t start = 0;
+    while (start < len) {
+        const uint64_t run = run_of(start);
+        int64_t a0 = start + 1, b0 = len;
+        while (a0 < b0) {
+            const int64_t mid = (a0 + b0) >> 1;
+            if (run_of(mid) == run) a0 = mid + 1;
+            else b0 = mid;
+        }
+        const int64_t end = a0;
+        for (int w = threadIdx.x; w < 256; w += kG2Threads) bm[w] = 0u;
+        __syncthreads();
+        for (int64_t r = start + threadIdx.x; r < end; r += kG2Threads) {
+            const uint32_t b = (ID[pget(src, r)] - id_base) & 8191u;
+            atomicOr(&bm[b >> 5], 1u << (b & 31u));
+            loc[b] = (uint16_t)(r - start);
+        }
+        __syncthreads();
+        const uint32_t c = threadIdx.x < 256 ? (uint32_t)__popc(bm[threadIdx.x]) : 0u;
+        const uint32_t ex = block_excl_scan<kG2Threads>(c, ws, nullptr);
+        if (threadIdx.x < 256) {
+            uint32_t bits = bm[threadIdx.x];
+            int64_t o = start + ex;
+            while (bits) {
+                const int b = __ffs(bits) - 1;
+                dst[o++] = pget(src, start + loc[threadIdx.x * 32 + b]);
+                bits &= bits - 1u;
+            }
+        }
+        __syncthreads();
+        start = end;
+    }
+    __threadfence_block();
+    __syncthreads();
 }
 
 __global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
@@ -806,14 +878,7 @@ __global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
         const int G = bin_hi - bin_lo;
         const int gb = G > 1 ? 32 - __clz(G - 1) : 0;    // bits of the bin index inside the chunk
         uint16_t* cur = nullptr;
-        if (hb == 0 && G <= 1) {
-            // one bucket (or empty): the L1 order (ids ascending) is final
-        } else if (hb + gb <= 8) {
-            // all remaining bits fit one stable 8-bit pass: (bin in chunk, bits below the digit)
-            cta_digit_pass<uint16_t, uint16_t>(sk, cur, pa, len, ChunkDigit{sp, (uint32_t)bin_lo, hb, 0},
-                                               reinterpret_cast<uint16_t*>(cnt), ws);
-            cur = pa;
-        } else {
+        if (len > 1) {   // (the L1 pass leaves ids unordered inside a bin: always sort)
             // (1) counting scatter on D <= 12 bits: (bin in chunk, top Dw varying bits below
             //     the digit); not stable, fixed in (2)
             const int Dw = min(12 - gb, hb);
@@ -888,7 +953,7 @@ __global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
                 for (int j = h; j < e; ++j) {
                     const uint32_t sj = src[j];
                     const uint64_t kj = sk[sj];
-                    rank += (kj < kv || (kj == kv && sj < me)) ? 1 : 0;
+                    rank += (kj < kv || (kj == kv && si[sj] < si[me])) ? 1 : 0;
                 }
                 dst[h + rank] = (uint16_t)me;
             }
@@ -897,32 +962,61 @@ __global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
             uint16_t* wc = reinterpret_cast<uint16_t*>(cnt);   // [kG2Warps][256] for the stable passes
             for (int q = 0; q < nl; ++q) {
                 const int h = lst[2 * q], e = lst[2 * q + 1];
+                // (key, id) order for a long segment: (1) position bitmap -> L1 order, whose
+                // (bin, tile) runs ascend; (2) rank by id inside each run (O(run length));
+                // (3) stable passes over the key bits below sh if they vary here
                 for (int w = threadIdx.x; w < kG2Cap / 32; w += kG2Threads) bm[w] = 0u;
                 __syncthreads();
                 uint64_t so = 0, sa = ~0ull;
                 for (int r = h + threadIdx.x; r < e; r += kG2Threads) {
-                    const uint32_t p = src[r];
-                    atomicOr(&bm[p >> 5], 1u << (p & 31u));
-                    const uint64_t k = sk[p];
-                    so |= k;
-                    sa &= k;
+                    const uint32_t pp = src[r];
+                    atomicOr(&bm[pp >> 5], 1u << (pp & 31u));
+                    so |= sk[pp];
+                    sa &= sk[pp];
                 }
                 __syncthreads();
-                const uint32_t c = threadIdx.x < kG2Cap / 32 ? (uint32_t)__popc(bm[threadIdx.x]) : 0u;
-                uint32_t ex = block_excl_scan<kG2Threads>(c, ws, nullptr);
-                if (threadIdx.x < kG2Cap / 32) {
-                    uint32_t bits = bm[threadIdx.x];
-                    uint32_t o2 = h + ex;
-                    while (bits) {
-                        const int b = __ffs(bits) - 1;
-                        dst[o2++] = (uint16_t)(threadIdx.x * 32 + b);
-                        bits &= bits - 1u;
+                {
+                    const uint32_t c = threadIdx.x < kG2Cap / 32 ? (uint32_t)__popc(bm[threadIdx.x]) : 0u;
+                    uint32_t ex = block_excl_scan<kG2Threads>(c, ws, nullptr);
+                    if (threadIdx.x < kG2Cap / 32) {
+                        uint32_t bits = bm[threadIdx.x];
+                        uint32_t o2 = h + ex;
+                        while (bits) {
+                            const int b = __ffs(bits) - 1;
+                            pa[o2++] = (uint16_t)(threadIdx.x * 32 + b);   // pa = spare (src consumed)
+                            bits &= bits - 1u;
+                        }
                     }
                 }
-                const uint64_t v = cta_varying_from(so, sa, red) & ((sh > 0) ? ((1ull << sh) - 1ull) : 0ull);
-                if (!v) continue;  // all keys equal: position order is the final order
+                __syncthreads();
+                auto run_of = [&](int r) {
+                    const uint32_t pp = pa[r];
+                    return ((uint64_t)l1_digit(sk[pp], sp) << 32) | ((si[pp] - a.id_base) >> 13);
+                };
+                for (int r = h + threadIdx.x; r < e; r += kG2Threads) {
+                    const uint64_t run = run_of(r);
+                    int rh = h, rb = r;          // first index of the run (runs ascend)
+                    while (rh < rb) {
+                        const int mid = (rh + rb) >> 1;
+                        if (run_of(mid) < run) rh = mid + 1;
+                        else rb = mid;
+                    }
+                    int re = r + 1, eb = e;       // one past its last index
+                    while (re < eb) {
+                        const int mid = (re + eb) >> 1;
+                        if (run_of(mid) == run) re = mid + 1;
+                        else eb = mid;
+                    }
+                    const uint32_t me = pa[r], idm = si[me];
+                    int rank = 0;
+                    for (int j = rh; j < re; ++j) rank += si[pa[j]] < idm ? 1 : 0;
+                    dst[rh + rank] = (uint16_t)me;
+                }
+                __syncthreads();
+                const uint64_t vk = cta_varying_from(so, sa, red) & ((sh > 0) ? ((1ull << sh) - 1ull) : 0ull);
+                if (!vk) continue;   // all keys equal: id order is final
                 uint16_t* c2 = dst + h;
-                cta_lsd<uint16_t, uint16_t>(sk, c2, dst + h, pa + h, e - h, sh, v, wc, ws);
+                cta_lsd<uint16_t, uint16_t, uint64_t>(sk, c2, dst + h, pa + h, e - h, sh, vk, wc, ws);
                 if (c2 != dst + h) {
                     for (int r = threadIdx.x; r < e - h; r += kG2Threads) dst[h + r] = c2[r];
                     __syncthreads();
@@ -938,10 +1032,17 @@ __global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
     uint32_t* wc = reinterpret_cast<uint32_t*>(g2_dsm);  // [kG2Warps][256] u32
     uint32_t* p0 = a.scratch + (int64_t)t * 2 * n + lo;
     uint32_t* p1 = p0 + n;
+    // (key, id) order: the L1 pass does not keep ids ordered inside a bin
     const uint64_t varying = cta_varying(gk, len, red);
     const int sh1 = varying ? 64 - __clzll((long long)varying) : 0;
     uint32_t* cur = nullptr;
-    if (varying) {
+    uint32_t* rbm = reinterpret_cast<uint32_t*>(g2_dsm + 16384);          // [256]
+    uint16_t* rloc = reinterpret_cast<uint16_t*>(g2_dsm + 16384 + 1024);   // [8192]
+    if (!varying) {
+        // one bucket: order by id (tile runs, bitmap per run)
+        cta_sort_tile_runs(gi, gk, sp, nullptr, p0, len, a.id_base, rbm, rloc, ws);
+        cur = p0;
+    } else {
         // stable 3-way split around the key at the middle position when it dominates
         const uint64_t pivot = gk[len / 2];
         if (threadIdx.x < 3) cls_cnt[threadIdx.x] = 0;
@@ -994,14 +1095,18 @@ __global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
             }
             __threadfence_block();
             __syncthreads();
-            // sort the "less" and "greater" parts (the equal part is already id-ordered)
-            const int64_t part_lo[2] = {0, nlt + neq};
-            const int64_t part_len[2] = {nlt, len - nlt - neq};
-            for (int q = 0; q < 2; ++q) {
+            // each part by id; the less / greater parts then by key (stable passes)
+            const int64_t part_lo[3] = {0, nlt, nlt + neq};
+            const int64_t part_len[3] = {nlt, neq, len - nlt - neq};
+            for (int q = 0; q < 3; ++q) {
                 if (part_len[q] <= 1) continue;
                 uint32_t* c = p0 + part_lo[q];
-                cta_lsd<uint32_t, uint32_t>(gk, c, p0 + part_lo[q], p1 + part_lo[q], part_len[q], sh1, varying, wc,
-                                            ws);
+                // the stable partition kept the tile-run structure: id order by tile runs
+                cta_sort_tile_runs(gi, gk, sp, c, p1 + part_lo[q], part_len[q], a.id_base, rbm, rloc, ws);
+                c = p1 + part_lo[q];
+                if (q != 1)
+                    cta_lsd<uint32_t, uint32_t>(gk, c, p0 + part_lo[q], p1 + part_lo[q], part_len[q], sh1, varying, wc,
+                                                ws);
                 if (c != p0 + part_lo[q]) {
                     for (int64_t r = threadIdx.x; r < part_len[q]; r += kG2Threads) p0[part_lo[q] + r] = c[r];
                     __threadfence_block();
@@ -1010,6 +1115,8 @@ __global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
             }
             cur = p0;
         } else {
+            cta_sort_tile_runs(gi, gk, sp, nullptr, p0, len, a.id_base, rbm, rloc, ws);
+            cur = p0;
             cta_lsd<uint32_t, uint32_t>(gk, cur, p0, p1, len, sh1, varying, wc, ws);
         }
     }
@@ -1075,7 +1182,8 @@ size_t group_spec_bytes() { return sizeof(L1Spec); }
 // table by the digit of spec[0..L).
 static cudaError_t l1_pass(const uint64_t* kin, const uint32_t* iin, uint64_t* kout, uint32_t* iout, int64_t n, int L,
                            const L1Spec* spec, int nb1, uint32_t id_base, GroupScratch& sc, int span, int nchunks,
-                           uint32_t* chunkbin, int num_sms, cudaStream_t s, bool hist_done = false) {
+                           uint32_t* chunkbin, int num_sms, cudaStream_t s, bool hist_done = false,
+                           bool stable = true) {
     const int T = (int)group_tiles(n);
     const dim3 g1(T, L);
     if (!hist_done) {
@@ -1099,15 +1207,22 @@ static cudaError_t l1_pass(const uint64_t* kin, const uint32_t* iin, uint64_t* k
     const int grid = (int)std::min<int64_t>(items, (int64_t)num_sms);
     cudaError_t e;
     if (!ids) {
-        e = cudaFuncSetAttribute(g1_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
-        if (e != cudaSuccess) return e;
-        g1_scatter<true><<<grid, kSThreads, sm1, s>>>(kin, nullptr, kout, iout, n, spec, nb1, sc.hist, sc.binstart, T,
-                                                      L, id_base, nst);
+        if (stable) {
+            e = cudaFuncSetAttribute(g1_scatter<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+            if (e != cudaSuccess) return e;
+            g1_scatter<true, true><<<grid, kSThreads, sm1, s>>>(kin, nullptr, kout, iout, n, spec, nb1, sc.hist,
+                                                                sc.binstart, T, L, id_base, nst);
+        } else {
+            e = cudaFuncSetAttribute(g1_scatter<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+            if (e != cudaSuccess) return e;
+            g1_scatter<true, false><<<grid, kSThreads, sm1, s>>>(kin, nullptr, kout, iout, n, spec, nb1, sc.hist,
+                                                                 sc.binstart, T, L, id_base, nst);
+        }
     } else {
-        e = cudaFuncSetAttribute(g1_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+        e = cudaFuncSetAttribute(g1_scatter<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
         if (e != cudaSuccess) return e;
-        g1_scatter<false><<<grid, kSThreads, sm1, s>>>(kin, iin, kout, iout, n, spec, nb1, sc.hist, sc.binstart, T,
-                                                       L, id_base, nst);
+        g1_scatter<false, true><<<grid, kSThreads, sm1, s>>>(kin, iin, kout, iout, n, spec, nb1, sc.hist, sc.binstart,
+                                                             T, L, id_base, nst);
     }
     count_launch();
     timing_end("group_scatter", s);
@@ -1167,7 +1282,7 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
     }
     const int nch = group_chunks(n);
     e = l1_pass(keys, nullptr, sc.keys_a, sc.ids_a, n, L, spec, nb1, id_base, sc, kG2Span, nch, sc.chunkbin, sc.num_sms, s,
-                true);
+                true, /*stable=*/false);
     if (e != cudaSuccess) return e;
     timing_begin("group_sort", s);
     e = cudaMemsetAsync(sc.state, 0, sizeof(unsigned long long) * (size_t)L * nch, s);
@@ -1181,6 +1296,7 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
     a.spec = spec;
     a.n = n;
     a.nb1 = nb1;
+    a.id_base = id_base;
     a.nchunks = nch;
     a.chunkbin = sc.chunkbin;
     a.out = out;
