@@ -25,6 +25,8 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstdio>
 
 #include "internal.hpp"
 
@@ -357,9 +359,10 @@ constexpr int kSThreads = 512;
 constexpr int kSWarps = kSThreads / 32;
 constexpr int kSRounds = kG1Tile / kSThreads;   // 16
 
-size_t g1_scatter_smem(int nb1, bool ids, int nst) {
-    (void)ids;
-    return 64 + (size_t)nst * kG1Tile * 8 + (size_t)kG1Tile * 4 + (size_t)nb1 * 8 + (size_t)kSWarps * nb1 * 2;
+size_t g1_scatter_smem(int nb1, bool stable, int nst) {
+    // ring, staged permutation + digit, offsets, counters (per warp if stable)
+    return 64 + (size_t)nst * kG1Tile * 8 + (size_t)kG1Tile * 4 + (size_t)nb1 * 8 +
+           (stable ? (size_t)kSWarps * nb1 * 2 : (size_t)nb1 * 4);
 }
 
 // STABLE = false (wide-key MSD pass): ranks inside a digit come from one shared
@@ -438,7 +441,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
         uint64_t* kr = rk + (size_t)st * kG1Tile;
         const uint32_t* ir = IMPLICIT_IDS ? nullptr : iin + tb + (int64_t)tile * kG1Tile;
         g_mbar_wait(bars + st, phase);
-        for (int i = threadIdx.x; i < kSWarps * nb1; i += kSThreads) wrun[i] = 0;
+        for (int i = threadIdx.x; i < (STABLE ? kSWarps * nb1 : 2 * nb1); i += kSThreads) wrun[i] = 0;
         if (!bulk_ok(t, tile)) {
             for (int i = threadIdx.x; i < cnt; i += kSThreads) kr[i] = kin[tb + (int64_t)tile * kG1Tile + i];
         }
@@ -550,6 +553,7 @@ struct G2Args {
     int64_t n;
     int nb1;
     uint32_t id_base;           // ids of a table are id_base + row
+    unsigned long long* prof;   // diagnostics (LSH_G2_PROF): per-phase clock sums, nullptr = off
     int nchunks;                // L2 chunks per table
     const uint32_t* chunkbin;   // [L][nchunks+1] first L1 bin of every chunk
     IndexDev out;
@@ -833,7 +837,17 @@ __device__ void cta_sort_tile_runs(const uint32_t* ID, const uint64_t* K, const 
     __syncthreads();
 }
 
+#define G2_MARK(i)                                                             \
+    do {                                                                       \
+        if (a.prof && threadIdx.x == 0) {                                      \
+            const long long now = clock64();                                   \
+            atomicAdd(a.prof + (i), (unsigned long long)(now - g2_t0));        \
+            g2_t0 = now;                                                       \
+        }                                                                      \
+    } while (0)
+
 __global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
+    long long g2_t0 = clock64();
     extern __shared__ __align__(16) unsigned char g2_dsm[];
     __shared__ uint32_t ws[32];
     __shared__ uint32_t bc;
@@ -879,6 +893,7 @@ __global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
         const int gb = G > 1 ? 32 - __clz(G - 1) : 0;    // bits of the bin index inside the chunk
         uint16_t* cur = nullptr;
         if (len > 1) {   // (the L1 pass leaves ids unordered inside a bin: always sort)
+            G2_MARK(0);   // load
             // (1) counting scatter on D <= 12 bits: (bin in chunk, top Dw varying bits below
             //     the digit); not stable, fixed in (2)
             const int Dw = min(12 - gb, hb);
@@ -921,6 +936,7 @@ __global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
                 pa[(old >> hs) & 0xffffu] = (uint16_t)i;
             }
             __syncthreads();
+            G2_MARK(1);   // counting scatter
             // (2) order inside segments of equal key >> sh by (key, position): O(s) ranks for
             //     short segments; long ones by a position bitmap, then stable passes on the
             //     bits below sh if they vary there
@@ -958,6 +974,7 @@ __global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
                 dst[h + rank] = (uint16_t)me;
             }
             __syncthreads();
+            G2_MARK(2);   // segment ranks
             const int nl = min(nlst, kG2Long);
             uint16_t* wc = reinterpret_cast<uint16_t*>(cnt);   // [kG2Warps][256] for the stable passes
             for (int q = 0; q < nl; ++q) {
@@ -1024,7 +1041,9 @@ __global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
             }
             cur = dst;
         }
+        G2_MARK(3);   // long segments
         cta_emit<uint16_t>(sk, si, cur, len, lo, t, bin, a, ws, &bc);
+        G2_MARK(4);   // emit (incl. look-back)
         return;
     }
 
@@ -1169,7 +1188,13 @@ __global__ void __launch_bounds__(kG2Threads) g3_rle(const uint64_t* __restrict_
     }
 }
 
-static size_t g2_smem() { return (size_t)kG2Cap * 16 + (size_t)kG2Warps * 256 * 2; }
+// keys 8 + ids 4 + two u16 permutations per item, then the digit counters: 2048
+// words (12-bit window, two 16-bit counters per word), which also hold the per-warp
+// counts of the stable passes; the big path reuses the area for its own scratch
+static size_t g2_smem() {
+    const size_t cnt = std::max<size_t>(2048 * 4, (size_t)kG2Warps * 256 * 2);
+    return std::max<size_t>((size_t)kG2Cap * 16 + cnt, 16384 + 1024 + 16384);
+}
 
 size_t group_hist_words(int64_t n, int W) {
     return ((size_t)1 << group_l1_bits(n, W)) * group_tiles(n);
@@ -1202,7 +1227,7 @@ static cudaError_t l1_pass(const uint64_t* kin, const uint32_t* iin, uint64_t* k
     timing_begin("group_scatter", s);
     const bool ids = iin != nullptr;
     int nst = 2;
-    const size_t sm1 = g1_scatter_smem(nb1, ids, nst);
+    const size_t sm1 = g1_scatter_smem(nb1, stable || ids, nst);
     const int64_t items = (int64_t)T * L;
     const int grid = (int)std::min<int64_t>(items, (int64_t)num_sms);
     cudaError_t e;
@@ -1297,6 +1322,13 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
     a.n = n;
     a.nb1 = nb1;
     a.id_base = id_base;
+    a.prof = nullptr;
+    static unsigned long long* g2prof = nullptr;
+    if (getenv("LSH_G2_PROF")) {
+        if (!g2prof) cudaMalloc(&g2prof, 8 * sizeof(unsigned long long));
+        cudaMemsetAsync(g2prof, 0, 8 * sizeof(unsigned long long), s);
+        a.prof = g2prof;
+    }
     a.nchunks = nch;
     a.chunkbin = sc.chunkbin;
     a.out = out;
@@ -1305,6 +1337,16 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
     if (e != cudaSuccess) return e;
     g2_sort<<<dim3(L, nch), kG2Threads, sm2, s>>>(a);
     count_launch();
+    if (a.prof) {
+        unsigned long long h[8];
+        cudaMemcpyAsync(h, a.prof, sizeof h, cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        const double tot = (double)(h[0] + h[1] + h[2] + h[3] + h[4]) + 1e-9;
+        fprintf(stderr, "[g2 prof] chunks=%lld cycles/chunk: load %.0f  scatter %.0f  ranks %.0f  long %.0f  emit %.0f  (%.0f%% %.0f%% %.0f%% %.0f%% %.0f%%)\n",
+                (long long)L * nch, h[0] / (double)(L * nch), h[1] / (double)(L * nch), h[2] / (double)(L * nch),
+                h[3] / (double)(L * nch), h[4] / (double)(L * nch), 100 * h[0] / tot, 100 * h[1] / tot,
+                100 * h[2] / tot, 100 * h[3] / tot, 100 * h[4] / tot);
+    }
     timing_end("group_sort", s);
     return cudaGetLastError();
 }
