@@ -15,4 +15,9 @@ ncu --set full --clock-control none --import-source on -k "$K" -s 7 -c 7 -o gpur
 python tools/prof_hash.py --config C5 --scheme HCS_E2LSH --op hash --reps 1 --n 20000 > gpurun_out/p3.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:sketch -s 1 -c 1 -o gpurun_out/C5_HCS_E2LSH_full \
     python tools/prof_hash.py --config C5 --scheme HCS_E2LSH --op hash --reps 1 --n 20000 > gpurun_out/ncu3.log 2>&1
-echo done
+
+# summarize on the box (ncu reports are too large to copy back), keep the text evidence
+python tools/summarize_profiles.py round1 > gpurun_out/summarize.log 2>&1
+mkdir -p gpurun_out/profiles_box && cp -r profiles/* gpurun_out/profiles_box/
+mkdir -p gpurun_out/keep && mv gpurun_out/C5_HCS_E2LSH_full.ncu-rep gpurun_out/keep/ 2>/dev/null
+rm -f gpurun_out/*_full.ncu-rep
