@@ -463,7 +463,9 @@ __global__ void __launch_bounds__(kSThreads, 1)
             for (int r = 0; r < kSRounds; ++r) {
                 const int i = base + r * 32 + lane;
                 slot[r] = i < cnt ? l1_digit(kr[i], sp0) : 0x10000u + lane;
-                peers[r] = match_digit<11>(slot[r], nbits1, i < cnt);
+                // match.any: cheap when a warp sees few distinct digits (narrow,
+                // duplicate-heavy keys take this stable path)
+                peers[r] = __match_any_sync(0xffffffffu, slot[r]);
             }
 #pragma unroll
             for (int r = 0; r < kSRounds; ++r) {
