@@ -402,3 +402,34 @@ def test_hcs_slab_matches_generic_fallback(monkeypatch):
     r1 = parity.check_keys(p, ref, k1.view(np.uint64))
     r2 = parity.check_keys(p, ref, k2.view(np.uint64))
     assert r1["mismatch_outside_exempt"] == 0 and r2["mismatch_outside_exempt"] == 0, (r1, r2)
+
+
+@pytest.mark.parametrize("cfg,scheme,tables", [("C4", "CS_E2LSH", (0, 17, 63)), ("C4", "CS_SRP", (0, 31, 63)),
+                                               ("C5", "HCS_E2LSH", (0, 1, 128, 255))])
+def test_full_size_index_tables(cfg, scheme, tables):
+    """Index build at full n in the bench's launch configuration: selected tables are
+    bit-exact against the oracle's grouping of the same keys (tables rule, §5), and
+    bucket lookups of sampled points return their own buckets."""
+    c = synth.CONFIGS[cfg]
+    p = _params(c, scheme)
+    h = _handle(p)
+    X = synth.rows(c, 0, c.n, device="cuda")
+    idx = h.build_index(X, id_base=0)
+    keys = h.hash(X, keys=True)["keys"]
+    torch.cuda.synchronize()
+    h.check()
+    for tt in tables:
+        kt = keys[tt].view(torch.int64).cpu().numpy().view(np.uint64)[None, :]
+        ref = lsh.group(kt)[0]
+        ids, uk, of = (x.cpu().numpy() for x in idx.view(tt))
+        assert np.array_equal(uk.astype(np.uint64), ref.ukeys), tt
+        assert np.array_equal(of.astype(np.uint32), ref.offs), tt
+        assert np.array_equal(ids.astype(np.uint32), ref.ids), tt
+    rows = torch.from_numpy(np.random.default_rng(1).choice(c.n, 64, replace=False)).cuda()
+    b, e = h.query_buckets(idx, X[rows].contiguous())
+    b, e = b.cpu().numpy(), e.cpu().numpy()
+    for tt in tables:
+        ids = idx.view(tt)[0].cpu().numpy()
+        for qi, r in enumerate(rows.cpu().numpy()):
+            assert r in ids[b[qi, tt]:e[qi, tt]].tolist()
+    idx.close()
