@@ -151,6 +151,25 @@ void lsh_index_destroy(lsh_index* idx);
 lsh_status lsh_query_buckets(const lsh_handle* h, const lsh_index* idx, const float* Q,
                              int64_t nq, int64_t ld, int64_t* begin, int64_t* end, void* stream);
 
+/* Query completion ("collect the index of all the
+ * elements", §6 PAPER.md:2000-2003 top-k retrieval).  For each query: its L bucket
+ * ranges (as lsh_query_buckets), the bucket entries in table order capped at
+ * max_cand entries, distinct ids, exact re-rank against the indexed points and the
+ * top k.  Similarity: squared Euclidean distance, ascending, for the E2LSH family;
+ * cosine similarity, descending, for the SRP family (0 when a norm is 0); ties by
+ * ascending id (readings C1, C2 in DESIGN.md).
+ *   X       float [n][ldx] (device): the rows the index was built from; id i is row
+ *           i - id_base of X (the caller keeps X alive; the library reads it).
+ *   Q       float [nq][ldq] (device) queries, ldq >= d.
+ *   out_ids int64 [nq][k] (device): ids, -1 where fewer than k candidates.
+ *   out_score float [nq][k] (device): the scores (+inf / -inf in missing slots).
+ *   out_ncand int32 [nq] (device, nullable): distinct candidates examined.
+ * 1 <= k <= max_cand <= 8192 (LSH_EINVAL otherwise); ldx, ldq >= d (LSH_EDIM).
+ * Asynchronous on `stream`; temporaries are stream-ordered allocations. */
+lsh_status lsh_query_knn(const lsh_handle* h, const lsh_index* idx, const float* X, int64_t ldx, const float* Q,
+                         int64_t nq, int64_t ldq, int32_t k, int32_t max_cand, int64_t* out_ids, float* out_score,
+                         int32_t* out_ncand, void* stream);
+
 /* Coarse per-table histogram for the multi-GPU exchange (§8(e)): counts uint32
  * [L][2^B] (device, overwritten), bin = top B bits of the key's significant width
  * (64 for E2LSH fingerprints, K for SRP; the key itself when that width <= B).

@@ -402,3 +402,47 @@ def global_coarse_offsets(all_counts: np.ndarray, rank: int) -> np.ndarray:
                                   np.cumsum(totals, axis=1)[:, :-1]], axis=1)
     before_ranks = c[:rank].sum(axis=0) if rank > 0 else np.zeros_like(totals)
     return before_bins + before_ranks
+
+
+# ---------------------------------------------------------------------------
+# Query completion: candidates = the union of the query's L
+# buckets ("collect the index of all the elements"), exact re-rank, top-k
+# under the family's similarity (§6: Euclidean for the E2LSH family,
+# cosine for the SRP family).  Reading C1: the bucket entries are taken
+# in table order (t = 0..L-1, each bucket in ascending id), truncated to max_cand
+# entries BEFORE removing duplicates, so the cap is deterministic.  Reading C2:
+# scores are squared Euclidean distance (ascending) or cosine similarity
+# (descending; 0 when a norm is 0); ties by ascending id; missing slots id -1.
+# ---------------------------------------------------------------------------
+def query_candidates(tables: List[TableIndex], qkeys_q: Sequence[int], max_cand: int) -> np.ndarray:
+    """Distinct candidate ids of one query (ascending)."""
+    lst: List[int] = []
+    for t, tix in enumerate(tables):
+        b, e = lookup(tix, int(qkeys_q[t]))
+        lst.extend(int(v) for v in tix.ids[b:e])
+    return np.unique(np.asarray(lst[:max_cand], dtype=np.int64))
+
+
+def rerank(Xrows: np.ndarray, q: np.ndarray, cand: np.ndarray, k: int, metric: str) -> Tuple[np.ndarray, np.ndarray]:
+    """Top-k of `cand` (global ids; Xrows[i] is the row of candidate cand[i]) by exact fp64 score."""
+    Xr = np.asarray(Xrows, np.float64)
+    qq = np.asarray(q, np.float64)
+    if metric == "l2":
+        sc = ((Xr - qq[None, :]) ** 2).sum(axis=1)
+        order = np.lexsort((cand, sc))
+    else:
+        nx = np.sqrt((Xr ** 2).sum(axis=1))
+        nq = float(np.sqrt((qq ** 2).sum()))
+        dots = Xr @ qq
+        sc = np.where((nx > 0) & (nq > 0), dots / np.maximum(nx * nq, 1e-300), 0.0)
+        order = np.lexsort((cand, -sc))
+    ids = np.full(k, -1, np.int64)
+    scores = np.full(k, np.inf if metric == "l2" else -np.inf)
+    top = order[:k]
+    ids[: len(top)] = cand[top]
+    scores[: len(top)] = sc[top]
+    return ids, scores
+
+
+def metric_of(p: Params) -> str:
+    return "l2" if is_e2lsh(p.scheme) else "cosine"

@@ -60,6 +60,7 @@ def lib() -> ctypes.CDLL:
         "lsh_index_size": (i64, [vp]),
         "lsh_index_destroy": (None, [vp]),
         "lsh_query_buckets": (i32, [vp, vp, vp, i64, i64, vp, vp, vp]),
+        "lsh_query_knn": (i32, [vp, vp, vp, i64, vp, i64, i64, i32, i32, vp, vp, vp, vp]),
         "lsh_index_counts": (i32, [vp, i32, vp, vp]),
         "lsh_global_offsets": (i32, [vp, i32, i32, i32, i32, vp, vp]),
         "lsh_export_host": (i32, [P(lsh_params), i32, i32, vp, P(sz)]),
@@ -316,6 +317,21 @@ class LSH:
                                        begin.data_ptr() if nq else None, end.data_ptr() if nq else None,
                                        _stream_ptr(stream)), "lsh_query_buckets")
         return begin, end
+
+    def query_knn(self, index: Index, X, Q, k: int, max_cand: int = 4096, stream=None):
+        """Top-k of each query among the union of its L buckets (lsh_query_knn): ids int64
+        [nq, k] (-1 when missing), scores float32 [nq, k] (squared L2 for the E2LSH family,
+        cosine similarity for SRP), distinct candidates int32 [nq].  X = the indexed rows."""
+        torch = _torch()
+        nq, ldq = self._shape(Q)
+        _, ldx = self._shape(X)
+        ids = torch.empty((nq, k), dtype=torch.int64, device=Q.device)
+        sc = torch.empty((nq, k), dtype=torch.float32, device=Q.device)
+        nc = torch.empty((nq,), dtype=torch.int32, device=Q.device)
+        _check(lib().lsh_query_knn(self._h, index._ptr, X.data_ptr(), ldx, Q.data_ptr() if nq else None, nq, ldq,
+                                   k, max_cand, ids.data_ptr() if nq else None, sc.data_ptr() if nq else None,
+                                   nc.data_ptr() if nq else None, _stream_ptr(stream)), "lsh_query_knn")
+        return ids, sc, nc
 
     # -- parameters / status ------------------------------------------------
     def get_params(self, what: str, mode: int = 0):

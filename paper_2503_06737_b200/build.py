@@ -15,7 +15,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "liblsh_b200.so")
-SOURCES = ["api.cu", "sketch.cu", "sketch_chunked.cu", "sketch_hcs.cu", "group.cu", "dense.cu", "dense_tc.cu"]
+SOURCES = ["api.cu", "sketch.cu", "sketch_chunked.cu", "sketch_hcs.cu", "group.cu", "dense.cu", "dense_tc.cu", "knn.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

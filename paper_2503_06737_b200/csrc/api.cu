@@ -278,6 +278,7 @@ struct lsh_handle {
 struct lsh_index {
     const lsh_handle* h = nullptr;
     int64_t n = 0;
+    int64_t id_base = 0;
     int L = 0;
     IndexDev dev{};
     void* mem = nullptr;
@@ -819,6 +820,7 @@ extern "C" lsh_status lsh_group_keys(const lsh_handle* h, const uint64_t* keys, 
     lsh_index* I = nullptr;
     lsh_status st = alloc_index(h, n, s, &I);
     if (st != LSH_OK) return st;
+    I->id_base = id_base;
     st = group_impl(h, keys, nullptr, n, id_base, I, s);
     if (st != LSH_OK) {
         lsh_index_destroy(I);
@@ -846,6 +848,7 @@ extern "C" lsh_status lsh_build_index(const lsh_handle* h, const float* X, int64
             return cuda_fail(e, "keys alloc");
         }
     }
+    I->id_base = id_base;
     st = hash_impl(h, X, n, ld, HashOut{keys, nullptr, nullptr, nullptr}, s);
     if (st == LSH_OK) st = group_impl(h, keys, keys, n, id_base, I, s);
     if (keys) cudaFreeAsync(keys, s);
@@ -901,6 +904,33 @@ extern "C" lsh_status lsh_query_buckets(const lsh_handle* h, const lsh_index* id
         if (e != cudaSuccess) st = cuda_fail(e, "lookup");
     }
     cudaFreeAsync(qk, s);
+    return st;
+}
+
+extern "C" lsh_status lsh_query_knn(const lsh_handle* h, const lsh_index* idx, const float* X, int64_t ldx,
+                                    const float* Q, int64_t nq, int64_t ldq, int32_t k, int32_t max_cand,
+                                    int64_t* out_ids, float* out_score, int32_t* out_ncand, void* stream) {
+    if (!h || !idx || idx->h->p.L != h->p.L) return LSH_ESTATE;
+    if (k < 1 || max_cand < k || max_cand > 8192) return LSH_EINVAL;
+    if (nq < 0 || ldq < h->p.d || ldx < h->p.d) return LSH_EDIM;
+    if (nq == 0) return LSH_OK;
+    if (!X || !Q || !out_ids || !out_score) return LSH_EDIM;
+    CK(cudaSetDevice(h->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const int L = h->p.L;
+    int64_t* be = nullptr;
+    CK(cudaMallocAsync((void**)&be, sizeof(int64_t) * 2 * (size_t)nq * L, s));
+    lsh_status st = lsh_query_buckets(h, idx, Q, nq, ldq, be, be + (size_t)nq * L, stream);
+    if (st == LSH_OK) {
+        timing_begin("knn", s);
+        cudaError_t e = launch_knn(idx->dev, idx->n, L, (uint32_t)idx->id_base, be, be + (size_t)nq * L, X, ldx,
+                                   (int)h->p.d, Q, ldq, nq, k, max_cand, is_e2lsh(h->p.scheme) ? 0 : 1, out_ids,
+                                   out_score, out_ncand, s);
+        count_launch();
+        timing_end("knn", s);
+        if (e != cudaSuccess) st = cuda_fail(e, "knn");
+    }
+    cudaFreeAsync(be, s);
     return st;
 }
 

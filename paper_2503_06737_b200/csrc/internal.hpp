@@ -139,6 +139,10 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
                          GroupScratch& sc, IndexDev& out, int* flags, cudaStream_t s);
 cudaError_t launch_lookup(const uint64_t* qkeys, int64_t nq, int L, int64_t n, const IndexDev& idx,
                           int64_t* begin, int64_t* end, cudaStream_t s);
+cudaError_t launch_knn(const IndexDev& idx, int64_t n, int L, uint32_t id_base, const int64_t* begin,
+                       const int64_t* end, const float* X, int64_t ldx, int d, const float* Q, int64_t ldq,
+                       int64_t nq, int k, int max_cand, int cosine, int64_t* out_ids, float* out_score,
+                       int32_t* out_ncand, cudaStream_t s);
 cudaError_t launch_global_offsets(const uint32_t* all, int G, int rank, int L, int B, int64_t* off, cudaStream_t s);
 cudaError_t launch_counts(const IndexDev& idx, int64_t n, int L, int width, int B, uint32_t* counts,
                           cudaStream_t s);

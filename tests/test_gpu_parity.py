@@ -433,3 +433,79 @@ def test_full_size_index_tables(cfg, scheme, tables):
         for qi, r in enumerate(rows.cpu().numpy()):
             assert r in ids[b[qi, tt]:e[qi, tt]].tolist()
     idx.close()
+
+
+def _knn_check(p, X, Q, k, max_cand, rtol=1e-4):
+    """GPU query_knn vs the oracle's union/rerank on the same keys (NEXT-1)."""
+    h = _handle(p)
+    idx = h.build_index(X, id_base=0)
+    ids, sc, nc = h.query_knn(idx, X, Q, k, max_cand=max_cand)
+    torch.cuda.synchronize()
+    keys = h.hash(X, keys=True)["keys"].view(torch.int64).cpu().numpy().view(np.uint64)
+    qkeys = h.hash(Q, keys=True)["keys"].view(torch.int64).cpu().numpy().view(np.uint64)
+    tables = lsh.group(keys, id_base=0)
+    Xn, Qn = X.cpu().numpy(), Q.cpu().numpy()
+    ids, sc, nc = ids.cpu().numpy(), sc.cpu().numpy(), nc.cpu().numpy()
+    metric = lsh.metric_of(p)
+    stats = {"queries": Q.shape[0], "empty": 0, "ties": 0}
+    for qi in range(Q.shape[0]):
+        cand = lsh.query_candidates(tables, qkeys[:, qi], max_cand)
+        assert nc[qi] == len(cand), qi
+        if len(cand) == 0:
+            stats["empty"] += 1
+            assert (ids[qi] == -1).all()
+            continue
+        rid, rsc = lsh.rerank(Xn[cand], Qn[qi], cand, k, metric)
+        kk = min(k, len(cand))
+        assert (ids[qi, kk:] == -1).all() and (ids[qi, :kk] >= 0).all(), qi
+        assert set(ids[qi, :kk].tolist()) <= set(cand.tolist()), qi
+        # every reported score is the exact score of that id within the fp32 tolerance
+        aid, asc = lsh.rerank(Xn[cand], Qn[qi], cand, len(cand), metric)
+        full = dict(zip(aid.tolist(), asc.tolist()))
+        for j in range(kk):
+            ref = full[int(ids[qi, j])]
+            assert abs(sc[qi, j] - ref) <= rtol * max(1.0, abs(ref)), (qi, j, sc[qi, j], ref)
+        # same top-k except near-ties at the k-th score
+        kth = rsc[kk - 1]
+        band = rtol * max(1.0, abs(kth))
+        sure = {int(i) for i, s in zip(cand.tolist(), [full[c] for c in cand.tolist()])
+                if (s < kth - band if metric == "l2" else s > kth + band)}
+        got = set(ids[qi, :kk].tolist())
+        assert sure <= got, (qi, sure - got)
+        stats["ties"] += int(got != set(rid[:kk].tolist()))
+    idx.close()
+    return stats
+
+
+@pytest.mark.parametrize("cfg,scheme,k,max_cand", [("C2", "CS_E2LSH", 10, 4096), ("C2", "CS_SRP", 20, 512),
+                                                   ("C3", "HCS_E2LSH", 10, 2048), ("C3", "HCS_SRP", 5, 8192),
+                                                   ("C1", "CS_E2LSH", 7, 64)])
+def test_query_knn_matches_oracle(cfg, scheme, k, max_cand):
+    """NEXT-1 query completion: union of the L buckets (table order, capped), distinct ids,
+    exact re-rank, top-k (squared L2 for E2LSH, cosine for SRP), ties by id."""
+    c = synth.CONFIGS[cfg]
+    p = _params(c, scheme)
+    n = min(c.n, 8000)
+    X = synth.rows(c, 0, n, device="cuda")
+    g = torch.Generator(device="cuda").manual_seed(11)
+    Q = torch.cat([X[:40], X[100:140] + 0.01 * torch.randn((40, c.d), device="cuda", generator=g),
+                   synth.gaussian_rows_like(8, c.d, 123, device="cuda") * 50.0]).contiguous()
+    st = _knn_check(p, X, Q, k, max_cand)
+    assert st["empty"] < Q.shape[0]
+
+
+def test_query_knn_self_is_first_and_errors():
+    import paper_2503_06737_b200 as pk
+    c = synth.CONFIGS["C2"]
+    p = _params(c, "CS_E2LSH")
+    h = _handle(p)
+    X = synth.rows(c, 0, 3000, device="cuda")
+    idx = h.build_index(X, id_base=0)
+    ids, sc, nc = h.query_knn(idx, X, X[:64].contiguous(), 3)
+    ids, sc = ids.cpu().numpy(), sc.cpu().numpy()
+    # a point's own row is at distance 0: first unless another row is identical (lower id)
+    for q in range(64):
+        assert sc[q, 0] == 0.0 and (ids[q, 0] == q or (X[ids[q, 0]] == X[q]).all().item())
+    with pytest.raises(pk.LshError):
+        h.query_knn(idx, X, X[:2].contiguous(), 9000, max_cand=9000)
+    idx.close()
