@@ -18,7 +18,7 @@
 namespace lshb {
 
 namespace {
-constexpr int kQT = 256;
+constexpr int kQT = 1024;   // 32 warps score candidates in parallel
 constexpr int kQW = kQT / 32;
 
 __device__ __forceinline__ uint32_t ord_f32(float f) {   // ascending float -> ascending uint
@@ -160,7 +160,25 @@ __global__ void __launch_bounds__(kQT) knn_kernel(KnnArgs a, int P) {
         if (a.vec) {
             const float4* x4 = reinterpret_cast<const float4*>(x);
             const float4* q4 = reinterpret_cast<const float4*>(q);
-            for (int c = lane; c < (a.d >> 2); c += 32) {
+            const int d4 = a.d >> 2;
+            float t0 = 0.f, t1 = 0.f;   // second accumulators: two independent chains
+            int c = lane;
+            for (; c + 32 < d4; c += 64) {
+                const float4 xv = __ldg(x4 + c), qv = __ldg(q4 + c);
+                const float4 xw = __ldg(x4 + c + 32), qw = __ldg(q4 + c + 32);
+                if (a.cosine) {
+                    s0 = fmaf(xv.x, qv.x, fmaf(xv.y, qv.y, fmaf(xv.z, qv.z, fmaf(xv.w, qv.w, s0))));
+                    s1 = fmaf(xv.x, xv.x, fmaf(xv.y, xv.y, fmaf(xv.z, xv.z, fmaf(xv.w, xv.w, s1))));
+                    t0 = fmaf(xw.x, qw.x, fmaf(xw.y, qw.y, fmaf(xw.z, qw.z, fmaf(xw.w, qw.w, t0))));
+                    t1 = fmaf(xw.x, xw.x, fmaf(xw.y, xw.y, fmaf(xw.z, xw.z, fmaf(xw.w, xw.w, t1))));
+                } else {
+                    const float d0 = xv.x - qv.x, d1 = xv.y - qv.y, d2 = xv.z - qv.z, d3 = xv.w - qv.w;
+                    const float e0 = xw.x - qw.x, e1 = xw.y - qw.y, e2 = xw.z - qw.z, e3 = xw.w - qw.w;
+                    s0 = fmaf(d0, d0, fmaf(d1, d1, fmaf(d2, d2, fmaf(d3, d3, s0))));
+                    t0 = fmaf(e0, e0, fmaf(e1, e1, fmaf(e2, e2, fmaf(e3, e3, t0))));
+                }
+            }
+            for (; c < d4; c += 32) {
                 const float4 xv = __ldg(x4 + c), qv = __ldg(q4 + c);
                 if (a.cosine) {
                     s0 = fmaf(xv.x, qv.x, fmaf(xv.y, qv.y, fmaf(xv.z, qv.z, fmaf(xv.w, qv.w, s0))));
@@ -170,6 +188,8 @@ __global__ void __launch_bounds__(kQT) knn_kernel(KnnArgs a, int P) {
                     s0 = fmaf(d0, d0, fmaf(d1, d1, fmaf(d2, d2, fmaf(d3, d3, s0))));
                 }
             }
+            s0 += t0;
+            s1 += t1;
         } else {
             for (int c = lane; c < a.d; c += 32) {
                 const float xv = __ldg(x + c), qv = __ldg(q + c);
