@@ -580,9 +580,9 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 // inspects 32 predecessors per step (lane 0 = nearest) and stops at the nearest
 // inclusive prefix.  Bins of a table are launched in increasing block order, so
 // predecessors are running.
-__device__ uint32_t chained_prefix_warp(unsigned long long* st, int b, uint32_t agg) {
+__device__ uint32_t chained_prefix_warp(unsigned long long* st, int b, uint32_t agg, bool published = false) {
     const int lane = threadIdx.x & 31;
-    if (lane == 0) st_release(st + b, ((b == 0 ? 2ull : 1ull) << 32) | agg);
+    if (lane == 0 && !published) st_release(st + b, ((b == 0 ? 2ull : 1ull) << 32) | agg);
     if (b == 0) return 0;
     uint32_t acc = 0;
     int j = b - 1;
@@ -723,9 +723,11 @@ __device__ void cta_lsd(const KE* K, PT*& cur, PT* b0, PT* b1, int64_t len, int 
 
 // Bucket count, chained numbering, and the outputs of one bin.  Each thread owns
 // a run of consecutive sorted positions: one block scan numbers the buckets.
+// `published`: this chunk's bucket count was already posted to the look-back state
+// (the id write-out by the other warps overlaps warp 0's look-back either way).
 template <typename PT>
 __device__ void cta_emit(const uint64_t* K, const uint32_t* ID, const PT* perm, int64_t len, int64_t lo, int t,
-                         int bin, const G2Args& a, uint32_t* ws, uint32_t* bc) {
+                         int bin, const G2Args& a, uint32_t* ws, uint32_t* bc, bool published = false) {
     const int64_t vp = (len + kG2Threads - 1) / kG2Threads;
     const int64_t r0 = min(len, (int64_t)threadIdx.x * vp), r1 = min(len, r0 + vp);
     uint32_t u = 0;
@@ -740,15 +742,16 @@ __device__ void cta_emit(const uint64_t* K, const uint32_t* ID, const PT* perm, 
     uint32_t utot;
     const uint32_t ex = block_excl_scan<kG2Threads>(u, ws, &utot);
     if (threadIdx.x < 32) {
-        const uint32_t pre = chained_prefix_warp(a.state + (int64_t)t * a.nchunks, bin, utot);
+        const uint32_t pre = chained_prefix_warp(a.state + (int64_t)t * a.nchunks, bin, utot, published);
         if (threadIdx.x == 0) *bc = pre;
     }
+    const int64_t n = a.n;
+    uint32_t* od = a.out.ids + (int64_t)t * n + lo;
+    for (int64_t r = threadIdx.x; r < len; r += kG2Threads) od[r] = ID[pget(perm, r)];
     __syncthreads();
     const uint32_t base = *bc;
-    const int64_t n = a.n;
     uint64_t* uk = a.out.ukeys + (int64_t)t * n;
     uint32_t* of = a.out.offs + (int64_t)t * (n + 1);
-    uint32_t* od = a.out.ids + (int64_t)t * n + lo;
     {
         uint32_t ub = base + ex;
         uint64_t prev = r0 > 0 ? K[pget(perm, r0 - 1)] : 0ull;
@@ -762,7 +765,6 @@ __device__ void cta_emit(const uint64_t* K, const uint32_t* ID, const PT* perm, 
             prev = k;
         }
     }
-    for (int64_t r = threadIdx.x; r < len; r += kG2Threads) od[r] = ID[pget(perm, r)];
     if (threadIdx.x == 0 && bin == a.nchunks - 1) {
         a.out.nb[t] = base + utot;
         of[base + utot] = (uint32_t)n;
@@ -857,6 +859,7 @@ __global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
     __shared__ int nlst;
     __shared__ unsigned long long red[2];
     __shared__ uint32_t cls_cnt[3];
+    __shared__ uint32_t s_heads;
     __shared__ uint32_t bm[kG2Cap / 32];
     // Work unit: chunk c = the whole L1 bins whose start lies in [c*S, (c+1)*S); its
     // items are contiguous and sorting them by the full key sorts them in place.
@@ -882,34 +885,54 @@ __global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
         uint16_t* pa = reinterpret_cast<uint16_t*>(g2_dsm + kG2Cap * 12);     // [cap]
         uint16_t* pb = pa + kG2Cap;                                           // [cap]
         uint32_t* cnt = reinterpret_cast<uint32_t*>(pb + kG2Cap);             // [2048] two u16 counters per word
-        for (int i = threadIdx.x; i < len; i += kG2Threads) {
-            sk[i] = gk[i];
-            si[i] = gi[i];
-        }
-        __syncthreads();
         // the bits below the L1 digit (the table's varying-bit mask chooses the window;
         // a chunk whose keys are constant there still sorts correctly, through the
         // long-segment path)
         const int hb = (sp.nbits == 0 || len == 0) ? 0 : 64 - __clzll((long long)sp.below);
         const int G = bin_hi - bin_lo;
         const int gb = G > 1 ? 32 - __clz(G - 1) : 0;    // bits of the bin index inside the chunk
-        uint16_t* cur = nullptr;
-        if (len > 1) {   // (the L1 pass leaves ids unordered inside a bin: always sort)
-            G2_MARK(0);   // load
-            // (1) counting scatter on D <= 12 bits: (bin in chunk, top Dw varying bits below
-            //     the digit); not stable, fixed in (2)
-            const int Dw = min(12 - gb, hb);
-            const int D = gb + Dw;
-            const int sh = hb - Dw;
-            const ChunkDigit cd{sp, (uint32_t)bin_lo, Dw, sh};
-            const int nw = (1 << D) > 2 ? (1 << D) >> 1 : 1;
-            for (int i = threadIdx.x; i < nw; i += kG2Threads) cnt[i] = 0u;
-            __syncthreads();
-            for (int i = threadIdx.x; i < len; i += kG2Threads) {
-                const uint32_t dg = cd(sk[i]);
-                atomicAdd(&cnt[dg >> 1], 1u << ((dg & 1u) << 4));
+        // (1) counting scatter on D <= 12 bits: (bin in chunk, top Dw varying bits below
+        //     the digit); not stable, fixed in (2).  Counted while the chunk is loaded.
+        const int Dw = min(12 - gb, hb);
+        const int D = gb + Dw;
+        const int sh = hb - Dw;
+        const ChunkDigit cd{sp, (uint32_t)bin_lo, Dw, sh};
+        const int nw = (1 << D) > 2 ? (1 << D) >> 1 : 1;
+        for (int i = threadIdx.x; i < nw; i += kG2Threads) cnt[i] = 0u;
+        if (threadIdx.x == 0) s_heads = 0u;
+        __syncthreads();
+        {
+            constexpr int PT = kG2Cap / kG2Threads / 2;   // 4 items per thread per half
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+                if (h2 * PT * kG2Threads >= len) break;
+                uint64_t kr[PT];
+                uint32_t ir[PT];
+#pragma unroll
+                for (int j = 0; j < PT; ++j) {
+                    const int i = threadIdx.x + (h2 * PT + j) * kG2Threads;
+                    if (i < len) {
+                        kr[j] = __ldg(gk + i);
+                        ir[j] = __ldg(gi + i);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < PT; ++j) {
+                    const int i = threadIdx.x + (h2 * PT + j) * kG2Threads;
+                    if (i < len) {
+                        sk[i] = kr[j];
+                        si[i] = ir[j];
+                        const uint32_t dg = cd(kr[j]);
+                        atomicAdd(&cnt[dg >> 1], 1u << ((dg & 1u) << 4));
+                    }
+                }
             }
-            __syncthreads();
+        }
+        __syncthreads();
+        uint16_t* cur = nullptr;
+        bool published = false;
+        if (len > 1) {   // (the L1 pass leaves ids unordered inside a bin: always sort)
+            G2_MARK(0);   // load + digit counts
             {
                 const int WPT = (nw + kG2Threads - 1) / kG2Threads;
                 uint32_t sm = 0;
@@ -947,6 +970,7 @@ __global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
             // after the scatter, counter word w holds the END positions of digits 2w, 2w+1;
             // a segment of equal key >> sh is exactly one digit bucket
             auto digit_end = [&](uint32_t dg) { return (cnt[dg >> 1] >> ((dg & 1u) << 4)) & 0xffffu; };
+            uint32_t heads = 0;
             for (int r = threadIdx.x; r < len; r += kG2Threads) {
                 const uint32_t me = src[r];
                 const uint64_t kv = sk[me];
@@ -955,6 +979,7 @@ __global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
                 const int h = dg ? (int)digit_end(dg - 1) : 0;
                 if (e - h == 1) {
                     dst[r] = (uint16_t)me;
+                    ++heads;
                     continue;
                 }
                 if (e - h > kG2Seg) {   // long segment: position bitmap below
@@ -967,15 +992,27 @@ __global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
                     }
                     continue;
                 }
+                const uint32_t idm = si[me];
                 int rank = 0;
+                bool dup = false;   // an equal key with a smaller id: not the bucket's head
                 for (int j = h; j < e; ++j) {
                     const uint32_t sj = src[j];
                     const uint64_t kj = sk[sj];
-                    rank += (kj < kv || (kj == kv && si[sj] < si[me])) ? 1 : 0;
+                    const bool eqs = kj == kv && si[sj] < idm;
+                    rank += (kj < kv || eqs) ? 1 : 0;
+                    dup |= eqs;
                 }
                 dst[h + rank] = (uint16_t)me;
+                heads += dup ? 0u : 1u;
             }
+            heads = __reduce_add_sync(0xffffffffu, heads);
+            if ((threadIdx.x & 31) == 0) atomicAdd(&s_heads, heads);
             __syncthreads();
+            // no long segment: every bucket head is known, so post this chunk's bucket
+            // count now; later chunks' look-backs need not wait for this chunk's emit
+            published = nlst == 0;
+            if (published && threadIdx.x == 0)
+                st_release(a.state + (int64_t)t * a.nchunks + bin, ((bin == 0 ? 2ull : 1ull) << 32) | s_heads);
             G2_MARK(2);   // segment ranks
             const int nl = min(nlst, kG2Long);
             uint16_t* wc = reinterpret_cast<uint16_t*>(cnt);   // [kG2Warps][256] for the stable passes
@@ -1044,7 +1081,7 @@ __global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
             cur = dst;
         }
         G2_MARK(3);   // long segments
-        cta_emit<uint16_t>(sk, si, cur, len, lo, t, bin, a, ws, &bc);
+        cta_emit<uint16_t>(sk, si, cur, len, lo, t, bin, a, ws, &bc, published);
         G2_MARK(4);   // emit (incl. look-back)
         return;
     }
