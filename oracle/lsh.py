@@ -22,6 +22,9 @@ uses coordinates [tK, (t+1)K); B2 sqrt(m) with m the total size; B3 one offset
 per coordinate; B6 0-based column-major; B7 logical zero padding; B9 floor
 toward -inf; B10 E2LSH bucket key = 64-bit fingerprint of the K codes; B11
 buckets in ascending unsigned key order, ids ascending inside a bucket.
+C3 (NEXT-2, per_table=True): table t has its own CS family (h_t, s_t, b_t) of
+size K drawn from streams "table{t}/...", g_t(p)_k = floor((sqrt(K) CS_t(p)_k +
+b_tk)/w) -- the literal reading of "L independent hash tables".
 """
 
 from __future__ import annotations
@@ -62,6 +65,7 @@ class Params:
     seed: int = 0
     mode_d: Tuple[int, ...] = field(default_factory=tuple)  # HCS only
     mode_m: Tuple[int, ...] = field(default_factory=tuple)  # HCS only
+    per_table: bool = False   # NEXT-2 (reading C3): L independent CS families of size K
 
     def __post_init__(self):
         if self.scheme not in SCHEMES:
@@ -72,6 +76,8 @@ class Params:
             raise ValueError("w must be > 0")
         if not is_e2lsh(self.scheme) and self.K > 64:
             raise ValueError("SRP keys hold at most 64 bits")
+        if self.per_table and self.scheme not in ("CS_E2LSH", "CS_SRP"):
+            raise ValueError("per-table families are defined here for the CS schemes only")
         if is_hcs(self.scheme):
             if len(self.mode_d) != len(self.mode_m) or not self.mode_d:
                 raise ValueError("HCS needs per-mode d_k and m_k")
@@ -91,8 +97,8 @@ class Params:
 class Tables:
     """Materialised random parameters of one hasher."""
 
-    h: List[np.ndarray]            # per mode: bucket table h_k[d_k]
-    s: List[np.ndarray]            # per mode: sign table s_k[d_k] in {+1,-1}
+    h: List[np.ndarray]            # per mode: bucket table h_k[d_k] (per_table: per table t, h_t[d] in [K])
+    s: List[np.ndarray]            # per mode: sign table s_k[d_k] in {+1,-1} (per_table: per table)
     b: np.ndarray                  # fp32 offsets, m values
     R: Optional[np.ndarray] = None  # dense only: m x d, bf16-exact values
 
@@ -102,6 +108,14 @@ def make_tables(p: Params) -> Tables:
     if is_dense(p.scheme):
         R = rng.gaussian_rows(p.seed, p.m, p.d)
         return Tables(h=[], s=[], b=rng.offsets(p.seed, p.m, p.w), R=R)
+    if p.per_table:
+        # reading C3 ("L independent hash tables"; SURVEY 8(c) A1 "table{t}/"):
+        # table t draws its own h_t : [d] -> [K], s_t and b_t[K] from streams "table{t}/..."
+        pre = [f"table{t}/" for t in range(p.L)]
+        h = [rng.bucket_table(p.seed, 0, p.d, p.K, pre[t]) for t in range(p.L)]
+        s = [rng.sign_table(p.seed, 0, p.d, pre[t]) for t in range(p.L)]
+        b = np.concatenate([rng.offsets(p.seed, p.K, p.w, pre[t]) for t in range(p.L)])
+        return Tables(h=h, s=s, b=b)
     h = [rng.bucket_table(p.seed, k, dk, mk) for k, (dk, mk) in enumerate(zip(p.mode_d, p.mode_m))]
     s = [rng.sign_table(p.seed, k, dk) for k, dk in enumerate(p.mode_d)]
     return Tables(h=h, s=s, b=rng.offsets(p.seed, p.m, p.w))
@@ -171,6 +185,9 @@ def dense_project(X: np.ndarray, R: np.ndarray, ops: Optional[list] = None) -> n
 
 
 def project(p: Params, t: Tables, X: np.ndarray) -> np.ndarray:
+    if p.per_table:
+        # table t: its own count sketch of size K; coordinates [tK, (t+1)K) of the code
+        return np.concatenate([cs_sketch(X, t.h[tt], t.s[tt], p.K) for tt in range(p.L)], axis=1)
     if is_dense(p.scheme):
         return dense_project(X, t.R)
     if is_hcs(p.scheme):
@@ -183,7 +200,10 @@ def project(p: Params, t: Tables, X: np.ndarray) -> np.ndarray:
 # --------------------------------------------------------------------------
 
 def e2lsh_scale(p: Params) -> float:
-    """sqrt(m) for CS/HCS-E2LSH (reading B2); 1 for E2LSH."""
+    """sqrt(m) for CS/HCS-E2LSH (P:314, P:624, reading B2); 1 for E2LSH (P:169);
+    sqrt(K) for the per-table families, whose sketch size is K (reading C3)."""
+    if p.per_table:
+        return float(np.sqrt(p.K))
     return 1.0 if is_dense(p.scheme) else float(np.sqrt(p.m))
 
 
@@ -363,7 +383,9 @@ def param_count(p: Params) -> int:
     Dense: m*d Gaussians; CS: 2d table entries (bucket + sign); HCS: 2*sum d_k;
     plus m offsets for the E2LSH variants.
     """
-    if is_dense(p.scheme):
+    if p.per_table:
+        base = 2 * p.d * p.L
+    elif is_dense(p.scheme):
         base = p.m * p.d
     elif is_hcs(p.scheme):
         base = 2 * sum(p.mode_d)
@@ -380,7 +402,10 @@ def projection_op_count(p: Params, t: Tables, x: np.ndarray) -> int:
     """
     ops = [0]
     x = np.asarray(x, dtype=np.float64).reshape(1, -1)
-    if is_dense(p.scheme):
+    if p.per_table:
+        for tt in range(p.L):
+            cs_sketch(x, t.h[tt], t.s[tt], p.K, ops)
+    elif is_dense(p.scheme):
         dense_project(x, t.R, ops)
     elif is_hcs(p.scheme):
         hcs_sketch(x, p.mode_d, p.mode_m, t.h, t.s, ops)

@@ -86,24 +86,25 @@ class TwoWise:
         return [self.eval(i) for i in range(domain)]
 
 
-def bucket_table(seed: int, mode: int, d_k: int, m_k: int) -> np.ndarray:
-    """h_k : [d_k] -> [m_k] for mode k (k = 0 is the CS hash h), P:205 / P:212."""
-    fam = TwoWise(Stream(seed, f"mode{mode}/bucket"), m_k)
+def bucket_table(seed: int, mode: int, d_k: int, m_k: int, prefix: str = "") -> np.ndarray:
+    """h_k : [d_k] -> [m_k] for mode k (k = 0 is the CS hash h), P:205 / P:212.
+    `prefix` = "table{t}/" for the per-table families of NEXT-2 (reading C3)."""
+    fam = TwoWise(Stream(seed, f"{prefix}mode{mode}/bucket"), m_k)
     return np.array(fam.table(d_k), dtype=np.int64)
 
 
-def sign_table(seed: int, mode: int, d_k: int) -> np.ndarray:
+def sign_table(seed: int, mode: int, d_k: int, prefix: str = "") -> np.ndarray:
     """s_k : [d_k] -> {+1, -1}; parity 0 -> +1, parity 1 -> -1."""
-    fam = TwoWise(Stream(seed, f"mode{mode}/sign"), 2)
+    fam = TwoWise(Stream(seed, f"{prefix}mode{mode}/sign"), 2)
     return np.array([1 if fam.eval(i) == 0 else -1 for i in range(d_k)], dtype=np.int64)
 
 
-def offsets(seed: int, m: int, w: float) -> np.ndarray:
+def offsets(seed: int, m: int, w: float, prefix: str = "") -> np.ndarray:
     """b_l ~ U[0, w), one per coordinate (readings B3, B4, R3); fp32 values."""
     if not w > 0:
         raise ValueError("w must be > 0")
     w32 = np.float32(w)
-    st = Stream(seed, "offsets")
+    st = Stream(seed, f"{prefix}offsets")
     out = np.empty(m, dtype=np.float32)
     for l in range(m):
         u = st.unit53()
