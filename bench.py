@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true", help="diagnostic only: skip the nvidia-smi sampler")
+    ap.add_argument("--per-table", action="store_true",
+                    help="NEXT-2: per-table independent CS families (reading C3); not the headline workload")
     return ap.parse_args()
 
 
@@ -147,12 +149,12 @@ def ncu_traffic(config, scheme, kernel="sketch"):
 # reference arm: the oracle on host cores
 # --------------------------------------------------------------------------
 
-def oracle_step_sample(cfg, scheme, rows):
+def oracle_step_sample(cfg, scheme, rows, per_table=False):
     import numpy as np
     from oracle import lsh
     import synth
     kw = dict(mode_d=cfg.mode_d, mode_m=cfg.mode_m) if scheme.startswith("HCS") else {}
-    p = lsh.Params(scheme, d=cfg.d, m=cfg.m, L=cfg.L, K=cfg.K, w=cfg.w, seed=cfg.hash_seed, **kw)
+    p = lsh.Params(scheme, d=cfg.d, m=cfg.m, L=cfg.L, K=cfg.K, w=cfg.w, seed=cfg.hash_seed, per_table=per_table, **kw)
     X = synth.rows(cfg, 0, rows).numpy()
     t0 = time.perf_counter()
     t = lsh.make_tables(p) if not hasattr(oracle_step_sample, "_t") else oracle_step_sample._t
@@ -167,16 +169,20 @@ def cpu_sample_rows(cfg):
     return {"C1": cfg.n, "C2": 20000, "C3": 4000, "C4": 20000, "C5": 200}.get(cfg.name, 2000)
 
 
+def workload_name(cfg, args):
+    return f"{cfg.name}:{args.scheme}" + (":per_table" if args.per_table else "")
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
     import synth
     cfg = synth.CONFIGS[args.config]
-    rows = min(cfg.n, cpu_sample_rows(cfg))
+    rows = min(cfg.n, cpu_sample_rows(cfg) // (16 if args.per_table else 1))
     times = []
     for i in range(args.warmup + args.steps):
-        dt = oracle_step_sample(cfg, args.scheme, rows)
+        dt = oracle_step_sample(cfg, args.scheme, rows, args.per_table)
         if i >= args.warmup:
             times.append(dt)
     tstep = statistics.median(times)
@@ -184,7 +190,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tstep * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{cfg.name}:{args.scheme}", "n": cfg.n, "d": cfg.d, "m": cfg.m, "L": cfg.L,
+            "config": {"workload": workload_name(cfg, args), "n": cfg.n, "d": cfg.d, "m": cfg.m, "L": cfg.L,
                        "K": cfg.K, "w": cfg.w, "sample_rows_per_step": rows},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": f"first {rows} rows of {cfg.name} per step (hash + group), NumPy fp64"},
@@ -217,7 +223,8 @@ def run_ours(args):
     cfg = synth.CONFIGS[args.config]
     scheme = args.scheme
     kw = dict(mode_d=cfg.mode_d, mode_m=cfg.mode_m) if scheme.startswith("HCS") else {}
-    h = pk.LSH(scheme, cfg.d, cfg.m, cfg.L, cfg.K, cfg.w, cfg.hash_seed, device=dev.index, **kw)
+    h = pk.LSH(scheme, cfg.d, cfg.m, cfg.L, cfg.K, cfg.w, cfg.hash_seed, device=dev.index, per_table=args.per_table,
+               **kw)
     lo, hi = shard(cfg.n, rank, world)
     n_local = hi - lo
     X = synth.rows(cfg, lo, hi, device=dev)
@@ -340,11 +347,13 @@ def run_ours(args):
         return
 
     hbm_peak, peak_kind = peaks()
-    dense = scheme in ("E2LSH", "SRP")
+    dense = scheme in ("E2LSH", "SRP") or args.per_table
     kinfo = None
     if dense:
         # tensor-core dense baseline: algorithmic flops 2*n*m*d (the split into 3 bf16 terms
-        # triples the executed MMA work; reported separately)
+        # triples the executed MMA work; reported separately).  Per-table families (NEXT-2)
+        # run the same GEMM on the K-sparse +-1 matrix: their definitional work is only
+        # 2*n*L*d flops (one signed add per coordinate and table), also reported.
         g_ms, g_n = pk.timing_get("dense_gemm")
         avg = g_ms / max(1, g_n)
         flops = 2.0 * n_local * cfg.m * cfg.d
@@ -354,6 +363,8 @@ def run_ours(args):
                 "peak_kind": tf_kind, "unit": "TFLOP/s", "frac": (achieved / tf_peak) if achieved else None,
                 "flops_per_launch": flops, "executed_mma_flops_per_launch": 3 * flops, "traffic": None,
                 "avg_launch_ms": avg}
+        if args.per_table:
+            roof["sparse_definitional_flops_per_launch"] = 2.0 * n_local * cfg.L * cfg.d
     else:
         # Algorithmic bytes per launch of each kernel of the step:
         #   sketch        read the points (4d B) + write their L keys (8 B each)
@@ -388,16 +399,16 @@ def run_ours(args):
                 "sketch_bytes_per_point": 4 * cfg.d + 8 * cfg.L}
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        rows = min(cfg.n, cpu_sample_rows(cfg))
-        oracle_step_sample(cfg, scheme, min(rows, 256))  # warm caches / table draw
-        dt = oracle_step_sample(cfg, scheme, rows)
+        rows = min(cfg.n, cpu_sample_rows(cfg) // (16 if args.per_table else 1))
+        oracle_step_sample(cfg, scheme, min(rows, 256), args.per_table)  # warm caches / table draw
+        dt = oracle_step_sample(cfg, scheme, rows, args.per_table)
         cpu = {"value": rows / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"first {rows} rows of {cfg.name}, hash + group, NumPy fp64 (single-threaded)"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}:{scheme}", "n": cfg.n, "d": cfg.d, "m": cfg.m, "L": cfg.L,
+        "config": {"workload": workload_name(cfg, args), "n": cfg.n, "d": cfg.d, "m": cfg.m, "L": cfg.L,
                    "K": cfg.K, "w": cfg.w, "queries_per_step": NQ, "parallelism": f"points sharded x{world}",
                    "l2": "inputs (%.2f GB) larger than L2; no flush" % (cfg.n * cfg.d * 4 / 1e9)},
         "roofline": roof,

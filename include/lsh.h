@@ -95,8 +95,18 @@ typedef struct {
     float w;                        /* bucket width, > 0 (E2LSH family; ignored by SRP) */
     uint64_t seed;                  /* master seed of every random draw */
     int32_t device;                 /* CUDA device ordinal */
-    int32_t reserved;               /* must be 0 */
+    int32_t flags;                  /* LSH_FLAG_* bits; other bits must be 0 */
 } lsh_params;
+
+/* NEXT-2, reading C3: "L independent hash tables of m-sized
+ * hash codes" taken literally -- table t has its own count sketch of
+ * size K: h_t : [d] -> [K], s_t : [d] -> {+1,-1}, offsets b_t[K], drawn from the
+ * streams "table{t}/mode0/bucket", "table{t}/mode0/sign", "table{t}/offsets";
+ * code coordinate tK + k is floor((sqrt(K) CS_t(x)_k + b_tk) / w) (E2LSH) or
+ * [CS_t(x)_k > 0] (SRP).  CS schemes only (others: LSH_EUNSUPPORTED).  O(L d) adds
+ * per point; this build runs it as one tensor-core GEMM with the K-sparse +-1
+ * matrix [m][d] (exact in bf16) and the dense path's 3-term bf16 split of x. */
+#define LSH_FLAG_PER_TABLE 1
 
 typedef struct lsh_handle lsh_handle;  /* hasher: parameters resident on the device */
 typedef struct lsh_index lsh_index;    /* built (m, L) index, device-resident CSR per table */

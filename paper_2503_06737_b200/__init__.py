@@ -33,7 +33,7 @@ class lsh_params(ctypes.Structure):
     _fields_ = [("scheme", ctypes.c_int32), ("N", ctypes.c_int32), ("d", ctypes.c_int64),
                 ("mode_d", ctypes.c_int32 * MAX_MODES), ("mode_m", ctypes.c_int32 * MAX_MODES),
                 ("m", ctypes.c_int32), ("L", ctypes.c_int32), ("K", ctypes.c_int32), ("w", ctypes.c_float),
-                ("seed", ctypes.c_uint64), ("device", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("seed", ctypes.c_uint64), ("device", ctypes.c_int32), ("flags", ctypes.c_int32)]
 
 
 _lib = None
@@ -89,12 +89,17 @@ def _check(status: int, where: str):
         raise LshError(status, where, detail)
 
 
+FLAG_PER_TABLE = 1   # include/lsh.h LSH_FLAG_PER_TABLE
+
+
 def make_params(scheme: str, d: int, m: int, L: int, K: int, w: float = 4.0, seed: int = 0,
                 mode_d: Optional[Sequence[int]] = None, mode_m: Optional[Sequence[int]] = None,
-                device: int = 0) -> lsh_params:
+                device: int = 0, per_table: bool = False) -> lsh_params:
+    """per_table: NEXT-2 independent families per table (LSH_FLAG_PER_TABLE, reading C3)."""
     p = lsh_params()
     p.scheme = SCHEMES[scheme]
-    p.d, p.m, p.L, p.K, p.w, p.seed, p.device, p.reserved = d, m, L, K, w, seed, device, 0
+    p.d, p.m, p.L, p.K, p.w, p.seed, p.device = d, m, L, K, w, seed, device
+    p.flags = FLAG_PER_TABLE if per_table else 0
     if scheme.startswith("HCS"):
         if not mode_d or not mode_m or len(mode_d) != len(mode_m):
             raise ValueError("HCS needs mode_d and mode_m")
@@ -233,10 +238,11 @@ class LSH:
     """One hasher (lsh_handle): parameters drawn from `seed`, resident on `device`."""
 
     def __init__(self, scheme: str, d: int, m: int, L: int, K: int, w: float = 4.0, seed: int = 0,
-                 mode_d: Optional[Sequence[int]] = None, mode_m: Optional[Sequence[int]] = None, device: int = 0):
+                 mode_d: Optional[Sequence[int]] = None, mode_m: Optional[Sequence[int]] = None, device: int = 0,
+                 per_table: bool = False):
         self.scheme, self.d, self.m, self.L, self.K, self.w, self.seed = scheme, d, m, L, K, w, seed
-        self.mode_d, self.mode_m, self.device = mode_d, mode_m, device
-        self.params = make_params(scheme, d, m, L, K, w, seed, mode_d, mode_m, device)
+        self.mode_d, self.mode_m, self.device, self.per_table = mode_d, mode_m, device, per_table
+        self.params = make_params(scheme, d, m, L, K, w, seed, mode_d, mode_m, device, per_table)
         h = ctypes.c_void_p()
         _check(lib().lsh_create(ctypes.byref(self.params), ctypes.byref(h)), "lsh_create")
         self._h = h

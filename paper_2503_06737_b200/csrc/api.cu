@@ -157,7 +157,9 @@ static lsh_status validate(const lsh_params* p) {
     if ((int64_t)p->L * p->K != p->m) return LSH_EINVAL;
     if (!(p->w > 0.0f) || !std::isfinite(p->w)) return LSH_EINVAL;
     if (!is_e2lsh(p->scheme) && p->K > 64) return LSH_EINVAL;
-    if (p->reserved != 0) return LSH_EINVAL;
+    if (p->flags & ~LSH_FLAG_PER_TABLE) return LSH_EINVAL;
+    if ((p->flags & LSH_FLAG_PER_TABLE) && !(p->scheme == LSH_CS_E2LSH || p->scheme == LSH_CS_SRP))
+        return LSH_EUNSUPPORTED;
     if (is_hcs(p->scheme)) {
         if (p->N < 1 || p->N > LSH_MAX_MODES) return LSH_EINVAL;
         int64_t pd = 1, pm = 1;
@@ -183,7 +185,39 @@ struct HostTables {
     std::vector<uint16_t> R;                 // dense only, bf16 bits [m][d]
 };
 
+static bool is_per_table(const lsh_params* p) { return (p->flags & LSH_FLAG_PER_TABLE) != 0; }
+// dense projection matrix in the handle: the Gaussian R, or the per-table sign matrix
+static bool uses_R(const lsh_params* p) { return is_dense(p->scheme) || is_per_table(p); }
+
 static void draw(const lsh_params* p, HostTables& t, bool with_gaussian) {
+    if (is_per_table(p)) {
+        // reading C3: table t draws (h_t, s_t, b_t) from its own "table{t}/" streams; the
+        // matrix row tK + h_t(i), column i holds s_t(i) (bf16 +-1, exact)
+        t.N = p->L;
+        t.b.clear();
+        t.R.assign((size_t)p->m * p->d, 0);
+        for (int tt = 0; tt < p->L; ++tt) {
+            const std::string pre = "table" + std::to_string(tt) + "/";
+            TwoWise fb = bucket_family(p->seed, 0, (uint64_t)p->K, pre);
+            TwoWise fs = sign_family(p->seed, 0, pre);
+            std::vector<float> bt;
+            offsets(p->seed, p->K, p->w, bt, pre);
+            t.b.insert(t.b.end(), bt.begin(), bt.end());
+            std::vector<int32_t> hv(p->d), sv(p->d);
+            for (int64_t i = 0; i < p->d; ++i) {
+                hv[i] = (int32_t)fb.eval((uint64_t)i);
+                sv[i] = fs.eval((uint64_t)i) == 0 ? 1 : -1;
+                t.R[(size_t)(tt * p->K + hv[i]) * p->d + i] = sv[i] > 0 ? 0x3F80 : 0xBF80;
+            }
+            t.md.push_back(p->d);
+            t.mm.push_back(p->K);
+            t.fb.push_back(fb);
+            t.fs.push_back(fs);
+            t.h.push_back(std::move(hv));
+            t.s.push_back(std::move(sv));
+        }
+        return;
+    }
     offsets(p->seed, p->m, p->w, t.b);
     if (is_dense(p->scheme)) {
         t.N = 1;
@@ -606,7 +640,9 @@ extern "C" lsh_status lsh_create(const lsh_params* p, lsh_handle** out) {
     // offsets folded with w: c_off[l] = b_l / w; c_scale = sqrt(m)/w (CS/HCS) or 1/w (dense)
     std::vector<float> coff(m);
     for (int l = 0; l < m; ++l) coff[l] = (float)((double)H->host.b[l] / (double)p->w);
-    const double scale = is_dense(p->scheme) ? 1.0 : (double)sqrtf((float)m);
+    const double scale = is_dense(p->scheme) ? 1.0
+                         : is_per_table(p)   ? (double)sqrtf((float)p->K)   // reading C3: sketch size K
+                                             : (double)sqrtf((float)m);
     H->disc.e2lsh = is_e2lsh(p->scheme) ? 1 : 0;
     H->disc.c_scale = (float)(scale / (double)p->w);
     if ((e = cudaMalloc(&H->d_coff, sizeof(float) * m)) != cudaSuccess) return fail(cuda_fail(e, "malloc"));
@@ -618,7 +654,7 @@ extern "C" lsh_status lsh_create(const lsh_params* p, lsh_handle** out) {
     H->disc.flags = H->d_flags;
     if ((e = cudaMalloc(&H->d_b, sizeof(float) * m)) != cudaSuccess) return fail(cuda_fail(e, "malloc"));
     cudaMemcpy(H->d_b, H->host.b.data(), sizeof(float) * m, cudaMemcpyHostToDevice);
-    if (is_dense(p->scheme)) {
+    if (uses_R(p)) {
         const size_t bytes = sizeof(uint16_t) * H->host.R.size();
         if ((e = cudaMalloc(&H->d_R, bytes)) != cudaSuccess) return fail(cuda_fail(e, "malloc R"));
         if ((e = cudaMemcpy(H->d_R, H->host.R.data(), bytes, cudaMemcpyHostToDevice)) != cudaSuccess)
@@ -676,11 +712,27 @@ static lsh_status hash_impl(const lsh_handle* H, const float* X, int64_t n, int6
     if (out.codes && !is_e2lsh(p.scheme)) out.codes = nullptr;
     if (out.bits && is_e2lsh(p.scheme)) out.bits = nullptr;
     if (n == 0) return LSH_OK;
-    if (is_dense(p.scheme)) {
+    if (uses_R(&p)) {
+        static const bool simt = getenv("LSH_DENSE_SIMT") && getenv("LSH_DENSE_SIMT")[0] == '1';
+        static const bool unfused = getenv("LSH_DENSE_UNFUSED") && getenv("LSH_DENSE_UNFUSED")[0] == '1';
+        cudaError_t e;
+        if (!simt && !unfused && out.keys && !out.codes && !out.bits && !out.proj &&
+            dense_tc_fused_keys_ok(p.m, p.K)) {
+            // keys straight from the accumulators (fused epilogue): no [n][m] projection in HBM
+            const int64_t rows = std::min<int64_t>(n, (int64_t)dense_tc_rows_per_batch(H->d_pad));
+            uint16_t* A = nullptr;
+            CK(cudaMallocAsync((void**)&A, sizeof(uint16_t) * (size_t)rows * 3 * H->d_pad, s));
+            const std::string gname = std::string(tname) == "sketch" ? "dense_gemm" : "dense_gemm_query";
+            timing_begin(gname.c_str(), s);
+            e = launch_dense_tc(X, n, ld, (int)p.d, H->d_Rpad, p.m, H->d_pad, A, rows, nullptr, s, out.keys, p.K,
+                                &H->disc);
+            timing_end(gname.c_str(), s);
+            CK(cudaFreeAsync(A, s));
+            if (e != cudaSuccess) return cuda_fail(e, "dense_gemm");
+            return LSH_OK;
+        }
         float* Y = out.proj;
         if (!Y) CK(cudaMallocAsync((void**)&Y, sizeof(float) * (size_t)n * p.m, s));
-        cudaError_t e;
-        static const bool simt = getenv("LSH_DENSE_SIMT") && getenv("LSH_DENSE_SIMT")[0] == '1';
         if (simt) {  // CUDA-core cross-check kernel (tests only)
             timing_begin("dense_gemm_simt", s);
             e = launch_dense_gemm_f32(X, n, ld, H->d_R, p.m, (int)p.d, Y, s);
@@ -974,6 +1026,7 @@ static lsh_status export_from(const lsh_params* p, const HostTables& t, int32_t 
         case LSH_EXPORT_BUCKET:
         case LSH_EXPORT_SIGN:
         case LSH_EXPORT_COEFFS: {
+            // per-table families: `mode` = table index
             if (is_dense(p->scheme) || mode < 0 || mode >= t.N) return LSH_EINVAL;
             if (what == LSH_EXPORT_BUCKET) put(t.h[mode].data(), t.h[mode].size() * 4);
             else if (what == LSH_EXPORT_SIGN) put(t.s[mode].data(), t.s[mode].size() * 4);
@@ -985,11 +1038,11 @@ static lsh_status export_from(const lsh_params* p, const HostTables& t, int32_t 
         }
         case LSH_EXPORT_OFFSETS: put(t.b.data(), t.b.size() * 4); break;
         case LSH_EXPORT_GAUSSIAN:
-            if (!is_dense(p->scheme)) return LSH_EINVAL;
+            if (!uses_R(p)) return LSH_EINVAL;
             put(t.R.data(), t.R.size() * 2);
             break;
         case LSH_EXPORT_COORD: {
-            if (is_dense(p->scheme)) return LSH_EINVAL;
+            if (is_dense(p->scheme) || is_per_table(p)) return LSH_EINVAL;
             std::vector<int32_t> bin;
             std::vector<int8_t> sg;
             coordinate_map(p, t, bin, sg);

@@ -8,10 +8,13 @@
 // so Y = [x0|x1|x2] . [R|R|R]^T is ONE bf16 GEMM over K' = 3*d_pad with fp32
 // accumulation: every product is exact, only the fp32 accumulation rounds.
 //
-// Kernel shape (one output tile per CTA, warp-specialised, 192 threads):
+// Kernel shape (one output tile per CTA, warp-specialised, 576 threads):
 //   warp 0      TMA producer: A tile 128 x 64 and B tile BN x 64 (bf16, SW128) per stage
 //   warp 1      TMEM allocation + MMA issue (one elected thread, UMMA 128 x BN x 16)
-//   warps 2..5  epilogue: tcgen05.ld 32 lanes x 16 columns at a time -> Y (fp32)
+//   warps 2..17 epilogue: tcgen05.ld 32 lanes x 16 columns at a time -> Y (fp32), or
+//               (fused, KT > 0) the discretisation + table keys straight from TMEM:
+//               16/KT whole tables per load, only the keys [L][n] reach HBM
+//               (codes as the sketches compute them, discretize.cuh)
 // 4-stage smem ring with full/empty mbarriers; tcgen05.commit frees a stage and
 // finally signals the epilogue.
 #include <cuda.h>
@@ -19,13 +22,15 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "discretize.cuh"
 #include "internal.hpp"
 
 namespace lshb {
 
 namespace tc {
 constexpr int BM = 128, BK = 64, STAGES = 4;
-constexpr int THREADS = 192;
+constexpr int EPI_WARPS = 16;                 // 4 per TMEM lane quadrant, each a quarter of the columns
+constexpr int THREADS = 64 + 32 * EPI_WARPS;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -91,10 +96,17 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
 }
 }  // namespace tc
 
-template <int BN>
+// Fused key epilogue (KT > 0): keys of table t for local row r at keys[t * kstride + r].
+struct KeyEpi {
+    uint64_t* keys;
+    int64_t kstride;
+    DiscretizeDev dz;
+};
+
+template <int BN, int KT>
 __global__ void __launch_bounds__(tc::THREADS, 1)
     dense_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b, int n,
-                    int m, int d_pad, int nk, float* __restrict__ Y) {
+                    int m, int d_pad, int nk, float* __restrict__ Y, KeyEpi ke) {
     using namespace tc;
     constexpr uint32_t A_BYTES = BM * BK * 2;   // 16 KB
     constexpr uint32_t B_BYTES = BN * BK * 2;
@@ -171,10 +183,11 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         // epilogue: warp w reads TMEM lanes [32*(w%4), +32) = tile rows
         mbar_wait(tmem_full, 0);
         fence_after();
-        const int q = warp & 3;
+        const int q = warp & 3;                        // tcgen05.ld: lanes [32 (warp % 4), +32)
+        const int slice = (warp - 2) >> 2;             // column slice of this warp in its quadrant
         const int row = m_tile * BM + q * 32 + lane;
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 16) {
+        for (int c0 = slice * 16; c0 < BN; c0 += 16 * (EPI_WARPS / 4)) {
             uint32_t v[16];
             const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
             asm volatile(
@@ -184,6 +197,31 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                 : "r"(taddr));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             const int col = n_tile * BN + c0;
+            if constexpr (KT > 0) {
+                // 16 / KT tables: code l = col + j, table (col + j) / KT (tables never straddle)
+#pragma unroll
+                for (int tb = 0; tb < 16 / KT; ++tb) {
+                    const int l0 = col + tb * KT;
+                    if (l0 >= m) break;
+                    uint64_t f;
+                    if (ke.dz.e2lsh) {
+                        f = LSHB_FNV_OFFSET;
+#pragma unroll
+                        for (int kk = 0; kk < KT; ++kk) {
+                            const float q = fmaf(__uint_as_float(v[tb * KT + kk]), ke.dz.c_scale,
+                                                 __ldg(ke.dz.c_off + l0 + kk));
+                            f = (f ^ (uint64_t)(uint32_t)floor_code(q, ke.dz.flags)) * LSHB_FNV_PRIME;
+                        }
+                        f = fmix64_dev(f);
+                    } else {
+                        f = 0;
+#pragma unroll
+                        for (int kk = 0; kk < KT; ++kk) f |= (__uint_as_float(v[tb * KT + kk]) > 0.0f ? 1ull : 0ull) << kk;
+                    }
+                    if (row < n) ke.keys[(int64_t)(l0 / KT) * ke.kstride + row] = f;
+                }
+                continue;
+            }
             if (row < n) {
                 float* dst = Y + (int64_t)row * m + col;
                 if (col + 16 <= m && (m % 4) == 0) {
@@ -268,21 +306,43 @@ size_t dense_tc_rows_per_batch(int d_pad) {
     return rows;
 }
 
-template <int BN>
-static cudaError_t launch_tc_t(const CUtensorMap& ma, const CUtensorMap& mb, int n, int m, int d_pad, float* Y,
-                               cudaStream_t s) {
+template <int BN, int KT>
+static cudaError_t launch_tc_k(const CUtensorMap& ma, const CUtensorMap& mb, int n, int m, int d_pad, float* Y,
+                               const KeyEpi& ke, cudaStream_t s) {
     const size_t smem = (size_t)tc::STAGES * (tc::BM * tc::BK * 2 + BN * tc::BK * 2) + 1024 + 256;
-    cudaError_t e = cudaFuncSetAttribute(dense_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(dense_tc_kernel<BN, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int nk = 3 * d_pad / tc::BK;
     dim3 grid((m + BN - 1) / BN, (n + tc::BM - 1) / tc::BM);
-    dense_tc_kernel<BN><<<grid, tc::THREADS, smem, s>>>(ma, mb, n, m, d_pad, nk, Y);
+    dense_tc_kernel<BN, KT><<<grid, tc::THREADS, smem, s>>>(ma, mb, n, m, d_pad, nk, Y, ke);
     return cudaGetLastError();
 }
 
+template <int BN>
+static cudaError_t launch_tc_t(const CUtensorMap& ma, const CUtensorMap& mb, int n, int m, int d_pad, float* Y,
+                               const KeyEpi& ke, int K, cudaStream_t s) {
+    if (!ke.keys) return launch_tc_k<BN, 0>(ma, mb, n, m, d_pad, Y, ke, s);
+    switch (K) {
+        case 16: return launch_tc_k<BN, 16>(ma, mb, n, m, d_pad, Y, ke, s);
+        case 8: return launch_tc_k<BN, 8>(ma, mb, n, m, d_pad, Y, ke, s);
+        case 4: return launch_tc_k<BN, 4>(ma, mb, n, m, d_pad, Y, ke, s);
+        case 2: return launch_tc_k<BN, 2>(ma, mb, n, m, d_pad, Y, ke, s);
+        case 1: return launch_tc_k<BN, 1>(ma, mb, n, m, d_pad, Y, ke, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+bool dense_tc_fused_keys_ok(int m, int K) {
+    const int BN = m >= 256 ? 256 : (m > 128 ? ((m + 15) / 16) * 16 : 128);
+    return K >= 1 && K <= 16 && (16 % K) == 0 && (BN % K) == 0 && (m % K) == 0;
+}
+
 // Y [n][m] = X R^T with R_pad bf16 [m][d_pad] (zero padded), A scratch bf16 [rows][3*d_pad].
+// keys != nullptr: fused key epilogue (requires dense_tc_fused_keys_ok(m, K)), Y unused.
 cudaError_t launch_dense_tc(const float* X, int64_t n, int64_t ld, int d, const uint16_t* R_pad, int m, int d_pad,
-                            uint16_t* A_scratch, int64_t rows_per_batch, float* Y, cudaStream_t s) {
+                            uint16_t* A_scratch, int64_t rows_per_batch, float* Y, cudaStream_t s, uint64_t* keys,
+                            int K, const DiscretizeDev* dz) {
     if (n == 0) return cudaSuccess;
     CUtensorMap mb;
     const int BN = m >= 256 ? 256 : (m > 128 ? ((m + 15) / 16) * 16 : 128);
@@ -299,16 +359,23 @@ cudaError_t launch_dense_tc(const float* X, int64_t n, int64_t ld, int d, const 
         CUtensorMap ma;
         if (!make_map(&ma, A_scratch, (uint64_t)3 * d_pad, (uint64_t)nb, (uint64_t)3 * d_pad * 2, tc::BK, tc::BM))
             return cudaErrorInvalidValue;
+        KeyEpi ke{};
+        float* Yb = keys ? nullptr : Y + r0 * m;
+        if (keys) {
+            ke.keys = keys + r0;
+            ke.kstride = n;
+            ke.dz = *dz;
+        }
         cudaError_t e;
-        if (BN == 256) e = launch_tc_t<256>(ma, mb, (int)nb, m, d_pad, Y + r0 * m, s);
-        else if (BN == 128) e = launch_tc_t<128>(ma, mb, (int)nb, m, d_pad, Y + r0 * m, s);
-        else if (BN == 160) e = launch_tc_t<160>(ma, mb, (int)nb, m, d_pad, Y + r0 * m, s);
-        else if (BN == 192) e = launch_tc_t<192>(ma, mb, (int)nb, m, d_pad, Y + r0 * m, s);
-        else if (BN == 144) e = launch_tc_t<144>(ma, mb, (int)nb, m, d_pad, Y + r0 * m, s);
-        else if (BN == 176) e = launch_tc_t<176>(ma, mb, (int)nb, m, d_pad, Y + r0 * m, s);
-        else if (BN == 208) e = launch_tc_t<208>(ma, mb, (int)nb, m, d_pad, Y + r0 * m, s);
-        else if (BN == 224) e = launch_tc_t<224>(ma, mb, (int)nb, m, d_pad, Y + r0 * m, s);
-        else if (BN == 240) e = launch_tc_t<240>(ma, mb, (int)nb, m, d_pad, Y + r0 * m, s);
+        if (BN == 256) e = launch_tc_t<256>(ma, mb, (int)nb, m, d_pad, Yb, ke, K, s);
+        else if (BN == 128) e = launch_tc_t<128>(ma, mb, (int)nb, m, d_pad, Yb, ke, K, s);
+        else if (BN == 160) e = launch_tc_t<160>(ma, mb, (int)nb, m, d_pad, Yb, ke, K, s);
+        else if (BN == 192) e = launch_tc_t<192>(ma, mb, (int)nb, m, d_pad, Yb, ke, K, s);
+        else if (BN == 144) e = launch_tc_t<144>(ma, mb, (int)nb, m, d_pad, Yb, ke, K, s);
+        else if (BN == 176) e = launch_tc_t<176>(ma, mb, (int)nb, m, d_pad, Yb, ke, K, s);
+        else if (BN == 208) e = launch_tc_t<208>(ma, mb, (int)nb, m, d_pad, Yb, ke, K, s);
+        else if (BN == 224) e = launch_tc_t<224>(ma, mb, (int)nb, m, d_pad, Yb, ke, K, s);
+        else if (BN == 240) e = launch_tc_t<240>(ma, mb, (int)nb, m, d_pad, Yb, ke, K, s);
         else e = cudaErrorInvalidValue;
         count_launch();
         if (e != cudaSuccess) return e;

@@ -580,15 +580,23 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 // inspects 32 predecessors per step (lane 0 = nearest) and stops at the nearest
 // inclusive prefix.  Bins of a table are launched in increasing block order, so
 // predecessors are running.
-__device__ uint32_t chained_prefix_warp(unsigned long long* st, int b, uint32_t agg, bool published = false) {
+// `pre` (optional): the first round's values, loaded earlier by lookback_preload.
+__device__ __forceinline__ unsigned long long lookback_preload(const unsigned long long* st, int b) {
+    const int idx = b - 1 - (int)(threadIdx.x & 31);
+    return idx >= 0 ? ld_acquire(st + idx) : (2ull << 32);
+}
+__device__ uint32_t chained_prefix_warp(unsigned long long* st, int b, uint32_t agg, bool published = false,
+                                        const unsigned long long* pre = nullptr) {
     const int lane = threadIdx.x & 31;
     if (lane == 0 && !published) st_release(st + b, ((b == 0 ? 2ull : 1ull) << 32) | agg);
     if (b == 0) return 0;
     uint32_t acc = 0;
     int j = b - 1;
+    bool first = pre != nullptr;
     while (true) {
         const int idx = j - lane;
-        const unsigned long long v = idx >= 0 ? ld_acquire(st + idx) : (2ull << 32);
+        const unsigned long long v = first ? *pre : idx >= 0 ? ld_acquire(st + idx) : (2ull << 32);
+        first = false;
         const uint32_t f = (uint32_t)(v >> 32);
         const uint32_t incl = __ballot_sync(0xffffffffu, f == 2);
         const uint32_t notready = __ballot_sync(0xffffffffu, f == 0);
@@ -646,11 +654,17 @@ struct ShiftDigit {
     __device__ __forceinline__ uint32_t operator()(uint64_t k) const { return (uint32_t)(k >> sh) & 255u; }
 };
 // (L1 bin inside the chunk, the next `w` key bits below the L1 digit at shift `sh`)
+// A contiguous L1 digit sits directly above the window (its lowest bit is the top of
+// `below`), so (digit, window) is one bit field: shift, mask, subtract bin0.
 struct ChunkDigit {
     L1Spec sp;
     uint32_t bin0;
     int w, sh;
+    uint32_t fmask, fsub;
+    __device__ __forceinline__ ChunkDigit(const L1Spec& s, uint32_t b0, int w_, int sh_)
+        : sp(s), bin0(b0), w(w_), sh(sh_), fmask((1u << (w_ + s.nbits)) - 1u), fsub(b0 << w_) {}
     __device__ __forceinline__ uint32_t operator()(uint64_t k) const {
+        if (sp.shift >= 0) return ((uint32_t)(k >> sh) & fmask) - fsub;
         return ((l1_digit(k, sp) - bin0) << w) | ((uint32_t)(k >> sh) & ((1u << w) - 1u));
     }
 };
@@ -727,7 +741,8 @@ __device__ void cta_lsd(const KE* K, PT*& cur, PT* b0, PT* b1, int64_t len, int 
 // (the id write-out by the other warps overlaps warp 0's look-back either way).
 template <typename PT>
 __device__ void cta_emit(const uint64_t* K, const uint32_t* ID, const PT* perm, int64_t len, int64_t lo, int t,
-                         int bin, const G2Args& a, uint32_t* ws, uint32_t* bc, bool published = false) {
+                         int bin, const G2Args& a, uint32_t* ws, uint32_t* bc, bool published = false,
+                         const unsigned long long* pre = nullptr) {
     const int64_t vp = (len + kG2Threads - 1) / kG2Threads;
     const int64_t r0 = min(len, (int64_t)threadIdx.x * vp), r1 = min(len, r0 + vp);
     uint32_t u = 0;
@@ -742,8 +757,8 @@ __device__ void cta_emit(const uint64_t* K, const uint32_t* ID, const PT* perm, 
     uint32_t utot;
     const uint32_t ex = block_excl_scan<kG2Threads>(u, ws, &utot);
     if (threadIdx.x < 32) {
-        const uint32_t pre = chained_prefix_warp(a.state + (int64_t)t * a.nchunks, bin, utot, published);
-        if (threadIdx.x == 0) *bc = pre;
+        const uint32_t p0 = chained_prefix_warp(a.state + (int64_t)t * a.nchunks, bin, utot, published, pre);
+        if (threadIdx.x == 0) *bc = p0;
     }
     const int64_t n = a.n;
     uint32_t* od = a.out.ids + (int64_t)t * n + lo;
@@ -896,7 +911,7 @@ __global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
         const int Dw = min(12 - gb, hb);
         const int D = gb + Dw;
         const int sh = hb - Dw;
-        const ChunkDigit cd{sp, (uint32_t)bin_lo, Dw, sh};
+        const ChunkDigit cd(sp, (uint32_t)bin_lo, Dw, sh);
         const int nw = (1 << D) > 2 ? (1 << D) >> 1 : 1;
         for (int i = threadIdx.x; i < nw; i += kG2Threads) cnt[i] = 0u;
         if (threadIdx.x == 0) s_heads = 0u;
@@ -931,6 +946,7 @@ __global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
         __syncthreads();
         uint16_t* cur = nullptr;
         bool published = false;
+        unsigned long long lbpre = 0;
         if (len > 1) {   // (the L1 pass leaves ids unordered inside a bin: always sort)
             G2_MARK(0);   // load + digit counts
             {
@@ -1011,8 +1027,12 @@ __global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
             // no long segment: every bucket head is known, so post this chunk's bucket
             // count now; later chunks' look-backs need not wait for this chunk's emit
             published = nlst == 0;
-            if (published && threadIdx.x == 0)
-                st_release(a.state + (int64_t)t * a.nchunks + bin, ((bin == 0 ? 2ull : 1ull) << 32) | s_heads);
+            if (published && threadIdx.x < 32) {
+                if (threadIdx.x == 0)
+                    st_release(a.state + (int64_t)t * a.nchunks + bin, ((bin == 0 ? 2ull : 1ull) << 32) | s_heads);
+                // first look-back round issued now; consumed after the emit's scan
+                lbpre = lookback_preload(a.state + (int64_t)t * a.nchunks, bin);
+            }
             G2_MARK(2);   // segment ranks
             const int nl = min(nlst, kG2Long);
             uint16_t* wc = reinterpret_cast<uint16_t*>(cnt);   // [kG2Warps][256] for the stable passes
@@ -1081,7 +1101,7 @@ __global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
             cur = dst;
         }
         G2_MARK(3);   // long segments
-        cta_emit<uint16_t>(sk, si, cur, len, lo, t, bin, a, ws, &bc, published);
+        cta_emit<uint16_t>(sk, si, cur, len, lo, t, bin, a, ws, &bc, published, published ? &lbpre : nullptr);
         G2_MARK(4);   // emit (incl. look-back)
         return;
     }

@@ -104,7 +104,9 @@ bool hcs_plan_supported(int S, int M12);
 cudaError_t launch_dense_gemm_f32(const float* X, int64_t n, int64_t ld, const uint16_t* Rbf16, int m, int d,
                                   float* Y, cudaStream_t s);
 cudaError_t launch_dense_tc(const float* X, int64_t n, int64_t ld, int d, const uint16_t* R_pad, int m, int d_pad,
-                            uint16_t* A_scratch, int64_t rows_per_batch, float* Y, cudaStream_t s);
+                            uint16_t* A_scratch, int64_t rows_per_batch, float* Y, cudaStream_t s,
+                            uint64_t* keys = nullptr, int K = 0, const DiscretizeDev* dz = nullptr);
+bool dense_tc_fused_keys_ok(int m, int K);
 size_t dense_tc_rows_per_batch(int d_pad);
 cudaError_t launch_keys_from_proj(const float* Y, int64_t n, int m, int L, int K, const DiscretizeDev& disc,
                                   HashOut out, cudaStream_t s);

@@ -63,21 +63,22 @@ struct TwoWise {
     }
 };
 
-inline std::string mode_label(int k, const char* what) {
-    return "mode" + std::to_string(k) + "/" + what;
+// `prefix` = "table{t}/" for the per-table families (NEXT-2, reading C3).
+inline std::string mode_label(int k, const char* what, const std::string& prefix = "") {
+    return prefix + "mode" + std::to_string(k) + "/" + what;
 }
 
-inline TwoWise bucket_family(uint64_t seed, int k, uint64_t m_k) {
-    Stream st(seed, mode_label(k, "bucket"));
+inline TwoWise bucket_family(uint64_t seed, int k, uint64_t m_k, const std::string& prefix = "") {
+    Stream st(seed, mode_label(k, "bucket", prefix));
     return TwoWise(st, m_k);
 }
-inline TwoWise sign_family(uint64_t seed, int k) {
-    Stream st(seed, mode_label(k, "sign"));
+inline TwoWise sign_family(uint64_t seed, int k, const std::string& prefix = "") {
+    Stream st(seed, mode_label(k, "sign", prefix));
     return TwoWise(st, 2);
 }
 
-inline void offsets(uint64_t seed, int m, float w, std::vector<float>& out) {
-    Stream st(seed, "offsets");
+inline void offsets(uint64_t seed, int m, float w, std::vector<float>& out, const std::string& prefix = "") {
+    Stream st(seed, prefix + "offsets");
     out.resize(m);
     for (int l = 0; l < m; ++l) {
         double u = st.unit53();

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "discretize.cuh"
 #include "internal.hpp"
 
 namespace lshb {
@@ -40,35 +41,7 @@ __device__ __forceinline__ float ldg_stream_f1(const float* p) {
     return r;
 }
 
-__device__ __forceinline__ uint64_t fmix64_dev(uint64_t z) {
-    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
-    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
-    return z ^ (z >> 31);
-}
 
-// floor(q) as int32 with sticky overflow flags (DESIGN.md §K1 discretisation).
-// Fast path |q| < 2^22: q + 1.5*2^23 rounded toward -inf has floor(q) in its low
-// mantissa bits (exact in fp32).
-__device__ __forceinline__ int32_t floor_code(float q, int* flags) {
-    if (fabsf(q) < 4194304.0f) {
-        float r = __fadd_rd(q, 12582912.0f);
-        return __float_as_int(r) - 0x4B400000;
-    }
-    if (q != q) {
-        atomicOr(flags, 2);
-        return 0;
-    }
-    float fq = floorf(q);
-    if (fq >= 2147483648.0f) {
-        atomicOr(flags, 1);
-        return INT32_MAX;
-    }
-    if (fq < -2147483648.0f) {
-        atomicOr(flags, 1);
-        return INT32_MIN;
-    }
-    return (int32_t)fq;
-}
 
 // Discretise one bin and fold it into the running table key (shared by every
 // projection kernel so the arithmetic is identical across schemes).

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "discretize.cuh"
 #include "internal.hpp"
 
 namespace lshb {
@@ -38,28 +39,6 @@ __device__ __forceinline__ float ldg_stream_f1(const float* p) {
     float r;
     asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
     return r;
-}
-__device__ __forceinline__ uint64_t fmix64_c(uint64_t z) {
-    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
-    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
-    return z ^ (z >> 31);
-}
-__device__ __forceinline__ int32_t floor_code_c(float q, int* flags) {
-    if (fabsf(q) < 4194304.0f) return __float_as_int(__fadd_rd(q, 12582912.0f)) - 0x4B400000;
-    if (q != q) {
-        atomicOr(flags, 2);
-        return 0;
-    }
-    const float fq = floorf(q);
-    if (fq >= 2147483648.0f) {
-        atomicOr(flags, 1);
-        return INT32_MAX;
-    }
-    if (fq < -2147483648.0f) {
-        atomicOr(flags, 1);
-        return INT32_MIN;
-    }
-    return (int32_t)fq;
 }
 __device__ __forceinline__ float fmax_nan_abs_c(float a, float q) {
     float r;
@@ -263,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint32_t cnt = s_bp[lb + 1] - s_bp[lb];
                         for (uint32_t j = 0; j < cnt; ++j) acc += p2[j * 33];
                         p2 += cnt * 33;
-                        const int32_t z = floor_code_c(fmaf(acc, cs, s_coff[l]), dz.flags);
+                        const int32_t z = floor_code(fmaf(acc, cs, s_coff[l]), dz.flags);
                         f = (f ^ (uint64_t)(uint32_t)z) * LSHB_FNV_PRIME;
                         if (KT == 0 && dbg && valid && out.codes) out.codes[row * m + l] = z;
                     }
@@ -271,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else if (KT > 0 && KT <= 32) {
                 f = sbits;
             }
-            if (valid && out.keys) out.keys[(int64_t)t * n + row] = E2 ? fmix64_c(f) : f;
+            if (valid && out.keys) out.keys[(int64_t)t * n + row] = E2 ? fmix64_dev(f) : f;
         }
         if (!has_next) break;
         columns_for_chunk(cn);

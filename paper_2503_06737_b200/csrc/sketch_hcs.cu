@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "discretize.cuh"
 #include "internal.hpp"
 
 namespace lshb {
@@ -28,28 +29,6 @@ namespace {
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 
-__device__ __forceinline__ uint64_t fmix64_h(uint64_t z) {
-    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
-    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
-    return z ^ (z >> 31);
-}
-__device__ __forceinline__ int32_t floor_code_h(float q, int* flags) {
-    if (fabsf(q) < 4194304.0f) return __float_as_int(__fadd_rd(q, 12582912.0f)) - 0x4B400000;
-    if (q != q) {
-        atomicOr(flags, 2);
-        return 0;
-    }
-    const float fq = floorf(q);
-    if (fq >= 2147483648.0f) {
-        atomicOr(flags, 1);
-        return INT32_MAX;
-    }
-    if (fq < -2147483648.0f) {
-        atomicOr(flags, 1);
-        return INT32_MIN;
-    }
-    return (int32_t)fq;
-}
 // a + sum of the cnt staged words listed at wo[0..cnt) (lane-relative base p); two
 // independent chains, the second half of each pair predicated
 __device__ __forceinline__ float sum_bin(float a, const float* p, const uint16_t* wo, uint32_t cnt) {
@@ -229,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int l = g * M12 + b;
             uint32_t zc;
             if constexpr (E2) {
-                zc = (uint32_t)floor_code_h(fmaf(y, cs, s_coff[l]), dz.flags);
+                zc = (uint32_t)floor_code(fmaf(y, cs, s_coff[l]), dz.flags);
                 if (dbg && valid && out.codes) out.codes[row * m + l] = (int32_t)zc;
             } else {
                 zc = y > 0.0f ? 1u : 0u;
@@ -248,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if constexpr (E2) fp = (fp ^ (uint64_t)zc) * LSHB_FNV_PRIME;
                 else fp |= (uint64_t)zc << kk;
             }
-            if (valid && out.keys) out.keys[(int64_t)(g * tpb + tb) * n + row] = E2 ? fmix64_h(fp) : fp;
+            if (valid && out.keys) out.keys[(int64_t)(g * tpb + tb) * n + row] = E2 ? fmix64_dev(fp) : fp;
         }
         return false;
     };

@@ -26,10 +26,25 @@ CODE_BAND = 1e-5
 SRP_BAND = 1e-6
 
 
+def on_tensor_cores(p: lsh.Params) -> bool:
+    """Dense schemes and the NEXT-2 per-table families run as the tcgen05 GEMM."""
+    return lsh.is_dense(p.scheme) or p.per_table
+
+
+def proj_matrix(p: lsh.Params, t: lsh.Tables) -> np.ndarray:
+    """[m][d] matrix the GEMM multiplies by: R, or the per-table +-1 block matrix."""
+    if lsh.is_dense(p.scheme):
+        return t.R.astype(np.float64)
+    M = np.zeros((p.m, p.d))
+    for tt in range(p.L):
+        M[tt * p.K + np.asarray(t.h[tt]), np.arange(p.d)] = np.asarray(t.s[tt], np.float64)
+    return M
+
+
 def sigma(p: lsh.Params, t: lsh.Tables, X: np.ndarray) -> np.ndarray:
     X2 = np.asarray(X, np.float64) ** 2
-    if lsh.is_dense(p.scheme):
-        return np.sqrt(X2 @ (t.R.astype(np.float64) ** 2).T)
+    if on_tensor_cores(p):
+        return np.sqrt(X2 @ (proj_matrix(p, t) ** 2).T)
     ones = [np.ones_like(s) for s in t.s]
     if lsh.is_hcs(p.scheme):
         return np.sqrt(lsh.hcs_sketch(X2, p.mode_d, p.mode_m, t.h, ones))
@@ -55,8 +70,8 @@ FP32_U = 2.0 ** -24
 def nnz_terms(p: lsh.Params, t: lsh.Tables, X: np.ndarray) -> np.ndarray:
     """Number of nonzero products in each projection entry."""
     nz = (np.asarray(X) != 0).astype(np.float64)
-    if lsh.is_dense(p.scheme):
-        return nz @ (t.R != 0).astype(np.float64).T
+    if on_tensor_cores(p):
+        return nz @ (proj_matrix(p, t) != 0).astype(np.float64).T
     ones = [np.ones_like(s) for s in t.s]
     if lsh.is_hcs(p.scheme):
         return lsh.hcs_sketch(nz, p.mode_d, p.mode_m, t.h, ones)
@@ -71,7 +86,7 @@ def tc_band_y(p: lsh.Params, t: lsh.Tables, X: np.ndarray) -> np.ndarray:
     Xa = np.abs(np.asarray(X, np.float64))
     d = Xa.shape[1]
     chunks = (np.add.reduceat((Xa != 0).astype(np.int64), np.arange(0, d, 16), axis=1) > 0).sum(axis=1)
-    abs_sum = Xa @ np.abs(t.R).T
+    abs_sum = Xa @ np.abs(proj_matrix(p, t)).T
     return 3.0 * chunks[:, None] * FP32_U * abs_sum
 
 
@@ -79,14 +94,14 @@ def code_band(p: lsh.Params, t: lsh.Tables, X: np.ndarray) -> np.ndarray:
     """Per-entry exemption half-width in quotient units (see module docstring)."""
     w = float(np.float32(p.w))
     derived = 6.0 * FP32_U * np.sqrt(nnz_terms(p, t, X)) * lsh.e2lsh_scale(p) * sigma(p, t, X) / w
-    if lsh.is_dense(p.scheme):
+    if on_tensor_cores(p):
         derived = np.maximum(derived, tc_band_y(p, t, X) / w)
     return np.maximum(CODE_BAND, derived)
 
 
 def srp_band(p: lsh.Params, t: lsh.Tables, X: np.ndarray) -> np.ndarray:
     derived = 6.0 * FP32_U * np.sqrt(nnz_terms(p, t, X)) * sigma(p, t, X)
-    if lsh.is_dense(p.scheme):
+    if on_tensor_cores(p):
         derived = np.maximum(derived, tc_band_y(p, t, X))
     return np.maximum(SRP_BAND, derived)
 

@@ -100,3 +100,32 @@ def test_no_undefined_internal_symbols():
     import subprocess
     out = subprocess.run(["nm", "-D", "--undefined-only", pk.LIB_PATH], capture_output=True, text=True).stdout
     assert "lshb" not in out, out
+
+
+@pytest.mark.parametrize("scheme,d,L,K,w,seed", [("CS_E2LSH", 100, 5, 8, 2.0, 3), ("CS_SRP", 37, 3, 4, 4.0, 12345)])
+def test_host_per_table_families_equal_oracle(scheme, d, L, K, w, seed):
+    # NEXT-2 (reading C3): the C++ host draw of every table's family and the +-1 matrix
+    pp = pk.make_params(scheme, d, L * K, L, K, w, seed, per_table=True)
+    op = lsh.Params(scheme, d=d, m=L * K, L=L, K=K, w=w, seed=seed, per_table=True)
+    ot = lsh.make_tables(op)
+    for t in range(L):
+        assert np.array_equal(pk.export_host(pp, "bucket", t), ot.h[t].astype(np.int32))
+        assert np.array_equal(pk.export_host(pp, "sign", t), ot.s[t].astype(np.int32))
+        co = pk.export_host(pp, "coeffs", t)
+        fb = rng.TwoWise(rng.Stream(seed, f"table{t}/mode0/bucket"), K)
+        fs = rng.TwoWise(rng.Stream(seed, f"table{t}/mode0/sign"), 2)
+        assert [int(x) for x in co] == [fb.a, fb.b, fs.a, fs.b]
+    off = pk.export_host(pp, "offsets")
+    assert np.array_equal(off.view(np.uint32), ot.b.view(np.uint32))
+    R = (pk.export_host(pp, "gaussian").astype(np.uint32) << 16).view(np.float32).reshape(L * K, d)
+    X = np.random.default_rng(0).standard_normal((3, d)).astype(np.float32)
+    np.testing.assert_allclose(X.astype(np.float64) @ R.astype(np.float64).T, lsh.project(op, ot, X), atol=1e-9)
+
+
+def test_per_table_flag_validation():
+    sz = ctypes.c_size_t(0)
+    p = pk.make_params("HCS_SRP", 16, 16, 1, 16, mode_d=(4, 4), mode_m=(4, 4), per_table=True)
+    assert pk.lib().lsh_export_host(ctypes.byref(p), 2, 0, None, ctypes.byref(sz)) == 7   # LSH_EUNSUPPORTED
+    p = pk.make_params("CS_SRP", 16, 16, 2, 8)
+    p.flags = 2
+    assert pk.lib().lsh_export_host(ctypes.byref(p), 2, 0, None, ctypes.byref(sz)) == 1   # unknown flag bit

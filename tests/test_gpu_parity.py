@@ -29,7 +29,7 @@ def _lib():
 def _handle(p: lsh.Params):
     import paper_2503_06737_b200 as pk
     kw = dict(mode_d=p.mode_d, mode_m=p.mode_m) if lsh.is_hcs(p.scheme) else {}
-    return pk.LSH(p.scheme, p.d, p.m, p.L, p.K, p.w, p.seed, **kw)
+    return pk.LSH(p.scheme, p.d, p.m, p.L, p.K, p.w, p.seed, per_table=p.per_table, **kw)
 
 
 def _params(cfg: synth.Config, scheme: str) -> lsh.Params:
@@ -509,3 +509,90 @@ def test_query_knn_self_is_first_and_errors():
     with pytest.raises(pk.LshError):
         h.query_knn(idx, X, X[:2].contiguous(), 9000, max_cand=9000)
     idx.close()
+
+
+# ---- NEXT-2: per-table independent families (reading C3) --------------------------
+
+def _pt_params(cfg: synth.Config, scheme: str) -> lsh.Params:
+    return lsh.Params(scheme, d=cfg.d, m=cfg.m, L=cfg.L, K=cfg.K, w=cfg.w, seed=cfg.hash_seed, per_table=True)
+
+
+@pytest.mark.parametrize("cfg,scheme", [("C1", "CS_E2LSH"), ("C1", "CS_SRP"), ("C2", "CS_E2LSH"), ("C2", "CS_SRP")])
+def test_per_table_config_full_n(cfg, scheme):
+    c = synth.CONFIGS[cfg]
+    p = _pt_params(c, scheme)
+    X = synth.rows(c, 0, c.n, device="cuda")
+    _compare(p, X, X.cpu().numpy())
+
+
+@pytest.mark.parametrize("n", [1, 33, 1000])
+@pytest.mark.parametrize("scheme,d,L,K", [("CS_E2LSH", 300, 5, 8), ("CS_SRP", 37, 3, 16), ("CS_E2LSH", 64, 24, 1)])
+def test_per_table_edge_shapes(n, scheme, d, L, K):
+    """m not a multiple of the GEMM's N tile, d not of 64, K = 1 (one bin per table)."""
+    p = lsh.Params(scheme, d=d, m=L * K, L=L, K=K, w=2.5, seed=7, per_table=True)
+    X = synth.gaussian_rows_like(n, d, 3, device="cuda")
+    _compare(p, X, X.cpu().numpy())
+
+
+def test_per_table_differs_from_shared_sketch():
+    """The flag really switches families: same seed, different keys than the shared sketch."""
+    c = synth.CONFIGS["C1"]
+    X = synth.rows(c, 0, 256, device="cuda")
+    kp = _handle(_pt_params(c, "CS_SRP")).hash(X, keys=True)["keys"].cpu().numpy()
+    ks = _handle(_params(c, "CS_SRP")).hash(X, keys=True)["keys"].cpu().numpy()
+    assert (kp != ks).mean() > 0.5
+
+
+@pytest.mark.parametrize("scheme", ["CS_E2LSH", "CS_SRP"])
+def test_per_table_build_index_and_knn(scheme):
+    c = synth.CONFIGS["C2"]
+    p = _pt_params(c, scheme)
+    h = _handle(p)
+    X = synth.rows(c, 0, c.n, device="cuda")
+    keys = h.hash(X, keys=True)["keys"].cpu().numpy()
+    idx = h.build_index(X, id_base=0)
+    _check_index(idx, lsh.group(keys), p.L)
+    idx.close()
+    _knn_check(p, X, X[:64], 10, 1024)
+
+
+@pytest.mark.parametrize("scheme", ["CS_E2LSH", "CS_SRP"])
+def test_per_table_c4_full_size_sampled(scheme):
+    """C4 shape (n = 1e6, d = 960, L = 64, K = 16) with per-table families, sampled rows."""
+    c = synth.CONFIGS["C4"]
+    p = _pt_params(c, scheme)
+    X = synth.rows(c, 0, c.n, device="cuda")
+    h = _handle(p)
+    out = h.hash(X, keys=True, proj=True)
+    torch.cuda.synchronize()
+    rows = np.concatenate([np.arange(512), np.array([131071, 500000, 999999])])
+    ri = torch.from_numpy(rows).cuda()
+    Xs = X[ri].cpu().numpy()
+    t = lsh.make_tables(p)
+    ref = lsh.hash_points(p, t, Xs)
+    pr = parity.check_proj(out["proj"][ri].cpu().numpy(), ref["proj"], parity.sigma(p, t, Xs))
+    assert pr["bad"] == 0 and pr["bad_empty"] == 0, pr
+    ref["band"] = parity.code_band(p, t, Xs) if lsh.is_e2lsh(p.scheme) else parity.srp_band(p, t, Xs)
+    kr = parity.check_keys(p, ref, out["keys"].view(torch.int64)[:, ri].cpu().numpy().view(np.uint64))
+    assert kr["mismatch_outside_exempt"] == 0, kr
+
+
+@pytest.mark.parametrize("scheme,d,m,L,K,per_table", [
+    ("E2LSH", 300, 160, 10, 16, False), ("SRP", 300, 48, 6, 8, False), ("E2LSH", 200, 1024, 64, 16, False),
+    ("CS_E2LSH", 960, 1024, 64, 16, True), ("CS_SRP", 100, 40, 10, 4, True), ("CS_E2LSH", 64, 24, 24, 1, True)])
+def test_fused_key_epilogue_equals_materialised(scheme, d, m, L, K, per_table):
+    """Keys from the GEMM's fused TMEM epilogue == keys from the materialised projection
+    (same accumulators, same discretisation), and == the oracle outside the bands."""
+    p = lsh.Params(scheme, d=d, m=m, L=L, K=K, w=2.0, seed=5, per_table=per_table)
+    h = _handle(p)
+    X = synth.gaussian_rows_like(1000, d, 4, device="cuda")
+    kf = h.hash(X, keys=True)["keys"].view(torch.int64).cpu().numpy()
+    km = h.hash(X, keys=True, proj=True)["keys"].view(torch.int64).cpu().numpy()
+    h.check()
+    assert np.array_equal(kf, km)
+    t = lsh.make_tables(p)
+    Xn = X.cpu().numpy()
+    ref = lsh.hash_points(p, t, Xn)
+    ref["band"] = parity.code_band(p, t, Xn) if lsh.is_e2lsh(p.scheme) else parity.srp_band(p, t, Xn)
+    kr = parity.check_keys(p, ref, kf.view(np.uint64))
+    assert kr["mismatch_outside_exempt"] == 0, kr
