@@ -8,7 +8,9 @@
 // so Y = [x0|x1|x2] . [R|R|R]^T is ONE bf16 GEMM over K' = 3*d_pad with fp32
 // accumulation: every product is exact, only the fp32 accumulation rounds.
 //
-// Kernel shape (one output tile per CTA, warp-specialised, 576 threads):
+// Kernel shape (persistent, one CTA per SM walking output tiles, warp-specialised,
+// 576 threads; two TMEM accumulator buffers so a tile's epilogue overlaps the
+// next tile's MMAs):
 //   warp 0      TMA producer: A tile 128 x 64 and B tile BN x 64 (bf16, SW128) per stage
 //   warp 1      TMEM allocation + MMA issue (one elected thread, UMMA 128 x BN x 16)
 //   warps 2..17 epilogue: tcgen05.ld 32 lanes x 16 columns at a time -> Y (fp32), or
@@ -111,24 +113,33 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     constexpr uint32_t A_BYTES = BM * BK * 2;   // 16 KB
     constexpr uint32_t B_BYTES = BN * BK * 2;
     constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-    constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+    // two accumulator buffers (the epilogue of tile i overlaps the MMAs of tile i+1)
+    constexpr uint32_t ACC_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+    constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment of every operand tile (SW128 atoms)
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
     uint64_t* empty = full + STAGES;
-    uint64_t* tmem_full = empty + STAGES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+    uint64_t* tmem_full = empty + STAGES;    // [2] accumulator ready (MMA commit)
+    uint64_t* tmem_empty = tmem_full + 2;    // [2] accumulator drained (one arrive per epilogue warp)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_tile = blockIdx.x, m_tile = blockIdx.y;  // n_tile over projection rows (m), m_tile over points
+    // persistent: tiles t = blockIdx.x + i * gridDim.x, column tiles fastest (the CTAs
+    // in flight share A row tiles and walk B in step, so both stay L2-resident)
+    const int ntn = (m + BN - 1) / BN;
+    const int ntiles = ntn * ((n + BM - 1) / BM);
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(tmem_full, 1);
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tmem_full[a], 1);
+            mbar_init(&tmem_empty[a], EPI_WARPS);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_a) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_b) : "memory");
@@ -145,98 +156,121 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            // TMA producer
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % STAGES;
-                const uint32_t ph = (kb / STAGES) & 1;
-                mbar_wait(&empty[s], ph ^ 1);
-                unsigned char* a_dst = smem + s * STAGE_BYTES;
-                unsigned char* b_dst = a_dst + A_BYTES;
-                mbar_expect_tx(&full[s], STAGE_BYTES);
-                tma_load_2d(a_dst, &tmap_a, &full[s], kb * BK, m_tile * BM);
-                tma_load_2d(b_dst, &tmap_b, &full[s], (kb * BK) % d_pad, n_tile * BN);
+            // TMA producer: one k-block stream across all of this CTA's tiles
+            uint32_t g = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                const int n_tile = tile % ntn, m_tile = tile / ntn;
+                for (int kb = 0; kb < nk; ++kb, ++g) {
+                    const int s = g % STAGES;
+                    const uint32_t ph = (g / STAGES) & 1;
+                    mbar_wait(&empty[s], ph ^ 1);
+                    unsigned char* a_dst = smem + s * STAGE_BYTES;
+                    unsigned char* b_dst = a_dst + A_BYTES;
+                    mbar_expect_tx(&full[s], STAGE_BYTES);
+                    tma_load_2d(a_dst, &tmap_a, &full[s], kb * BK, m_tile * BM);
+                    tma_load_2d(b_dst, &tmap_b, &full[s], (kb * BK) % d_pad, n_tile * BN);
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             // MMA issuer: UMMA_K = 16 (32 bytes of K per instruction)
             constexpr uint32_t idesc = idesc_bf16(BM, BN);
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % STAGES;
-                const uint32_t ph = (kb / STAGES) & 1;
-                mbar_wait(&full[s], ph);
+            uint32_t g = 0, i = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+                const uint32_t acc = i & 1;
+                mbar_wait(&tmem_empty[acc], ((i >> 1) & 1) ^ 1);   // the epilogue drained this buffer
                 fence_after();
-                const uint32_t a_addr = smem_u32(smem + s * STAGE_BYTES);
-                const uint32_t b_addr = a_addr + A_BYTES;
+                const uint32_t tmem_d = tmem_base + acc * ACC_COLS;
+                for (int kb = 0; kb < nk; ++kb, ++g) {
+                    const int s = g % STAGES;
+                    const uint32_t ph = (g / STAGES) & 1;
+                    mbar_wait(&full[s], ph);
+                    fence_after();
+                    const uint32_t a_addr = smem_u32(smem + s * STAGE_BYTES);
+                    const uint32_t b_addr = a_addr + A_BYTES;
 #pragma unroll
-                for (int k = 0; k < BK / 16; ++k) {
-                    const uint64_t ad = sw128_desc(a_addr + k * 32);
-                    const uint64_t bd = sw128_desc(b_addr + k * 32);
-                    umma_bf16(tmem_base, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+                    for (int k = 0; k < BK / 16; ++k) {
+                        const uint64_t ad = sw128_desc(a_addr + k * 32);
+                        const uint64_t bd = sw128_desc(b_addr + k * 32);
+                        umma_bf16(tmem_d, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+                    }
+                    umma_commit(&empty[s]);  // frees the stage when these MMAs complete
                 }
-                umma_commit(&empty[s]);  // frees the stage when these MMAs complete
+                umma_commit(&tmem_full[acc]);   // accumulator ready
             }
-            umma_commit(tmem_full);      // accumulator ready
         }
         __syncwarp();
     } else {
         // epilogue: warp w reads TMEM lanes [32*(w%4), +32) = tile rows
-        mbar_wait(tmem_full, 0);
-        fence_after();
         const int q = warp & 3;                        // tcgen05.ld: lanes [32 (warp % 4), +32)
         const int slice = (warp - 2) >> 2;             // column slice of this warp in its quadrant
-        const int row = m_tile * BM + q * 32 + lane;
+        uint32_t i = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+            const int n_tile = tile % ntn, m_tile = tile / ntn;
+            const uint32_t acc = i & 1;
+            mbar_wait(&tmem_full[acc], (i >> 1) & 1);
+            fence_after();
+            const int row = m_tile * BM + q * 32 + lane;
 #pragma unroll 1
-        for (int c0 = slice * 16; c0 < BN; c0 += 16 * (EPI_WARPS / 4)) {
-            uint32_t v[16];
-            const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-                : "r"(taddr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            const int col = n_tile * BN + c0;
-            if constexpr (KT > 0) {
-                // 16 / KT tables: code l = col + j, table (col + j) / KT (tables never straddle)
+            for (int c0 = slice * 16; c0 < BN; c0 += 16 * (EPI_WARPS / 4)) {
+                uint32_t v[16];
+                const uint32_t taddr = tmem_base + acc * ACC_COLS + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+                    "[%16];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                      "=r"(v[15])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                const int col = n_tile * BN + c0;
+                if constexpr (KT > 0) {
+                    // 16 / KT tables: code l = col + j, table (col + j) / KT (tables never straddle)
 #pragma unroll
-                for (int tb = 0; tb < 16 / KT; ++tb) {
-                    const int l0 = col + tb * KT;
-                    if (l0 >= m) break;
-                    uint64_t f;
-                    if (ke.dz.e2lsh) {
-                        f = LSHB_FNV_OFFSET;
+                    for (int tb = 0; tb < 16 / KT; ++tb) {
+                        const int l0 = col + tb * KT;
+                        if (l0 >= m) break;
+                        uint64_t f;
+                        if (ke.dz.e2lsh) {
+                            f = LSHB_FNV_OFFSET;
 #pragma unroll
-                        for (int kk = 0; kk < KT; ++kk) {
-                            const float q = fmaf(__uint_as_float(v[tb * KT + kk]), ke.dz.c_scale,
-                                                 __ldg(ke.dz.c_off + l0 + kk));
-                            f = (f ^ (uint64_t)(uint32_t)floor_code(q, ke.dz.flags)) * LSHB_FNV_PRIME;
+                            for (int kk = 0; kk < KT; ++kk) {
+                                const float qv = fmaf(__uint_as_float(v[tb * KT + kk]), ke.dz.c_scale,
+                                                      __ldg(ke.dz.c_off + l0 + kk));
+                                f = (f ^ (uint64_t)(uint32_t)floor_code(qv, ke.dz.flags)) * LSHB_FNV_PRIME;
+                            }
+                            f = fmix64_dev(f);
+                        } else {
+                            f = 0;
+#pragma unroll
+                            for (int kk = 0; kk < KT; ++kk)
+                                f |= (__uint_as_float(v[tb * KT + kk]) > 0.0f ? 1ull : 0ull) << kk;
                         }
-                        f = fmix64_dev(f);
-                    } else {
-                        f = 0;
-#pragma unroll
-                        for (int kk = 0; kk < KT; ++kk) f |= (__uint_as_float(v[tb * KT + kk]) > 0.0f ? 1ull : 0ull) << kk;
+                        if (row < n) ke.keys[(int64_t)(l0 / KT) * ke.kstride + row] = f;
                     }
-                    if (row < n) ke.keys[(int64_t)(l0 / KT) * ke.kstride + row] = f;
+                    continue;
                 }
-                continue;
-            }
-            if (row < n) {
-                float* dst = Y + (int64_t)row * m + col;
-                if (col + 16 <= m && (m % 4) == 0) {
+                if (row < n) {
+                    float* dst = Y + (int64_t)row * m + col;
+                    if (col + 16 <= m && (m % 4) == 0) {
 #pragma unroll
-                    for (int j = 0; j < 16; j += 4)
-                        *reinterpret_cast<float4*>(dst + j) = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
-                                                                          __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
-                } else {
+                        for (int j = 0; j < 16; j += 4)
+                            *reinterpret_cast<float4*>(dst + j) =
+                                make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
+                                            __uint_as_float(v[j + 3]));
+                    } else {
 #pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        if (col + j < m) dst[j] = __uint_as_float(v[j]);
+                        for (int j = 0; j < 16; ++j)
+                            if (col + j < m) dst[j] = __uint_as_float(v[j]);
+                    }
                 }
             }
+            // this warp is done with the buffer: let the MMA warp overwrite it
+            fence_before();
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[acc])) : "memory");
         }
-        fence_before();
     }
     __syncthreads();
     if (warp == 1) {
@@ -314,7 +348,11 @@ static cudaError_t launch_tc_k(const CUtensorMap& ma, const CUtensorMap& mb, int
         cudaFuncSetAttribute(dense_tc_kernel<BN, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int nk = 3 * d_pad / tc::BK;
-    dim3 grid((m + BN - 1) / BN, (n + tc::BM - 1) / tc::BM);
+    const int ntiles = ((m + BN - 1) / BN) * ((n + tc::BM - 1) / tc::BM);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = ntiles < sms ? ntiles : sms;   // persistent: one CTA per SM
     dense_tc_kernel<BN, KT><<<grid, tc::THREADS, smem, s>>>(ma, mb, n, m, d_pad, nk, Y, ke);
     return cudaGetLastError();
 }
