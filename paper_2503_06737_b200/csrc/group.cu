@@ -34,9 +34,6 @@ namespace lshb {
 
 constexpr int kG1Tile = 8192;                   // items per L1 tile
 constexpr int kG1Threads = 256;
-constexpr int kG1Warps = kG1Threads / 32;       // 8
-constexpr int kG1PerWarp = kG1Tile / kG1Warps;  // 512 consecutive items per warp
-constexpr int kG1Rounds = kG1PerWarp / 32;      // 16
 constexpr int kG2Threads = 512;
 constexpr int kG2Warps = kG2Threads / 32;       // 16
 constexpr int kG2Cap = 4096;                    // bin items sorted in shared memory
@@ -385,7 +382,6 @@ __global__ void __launch_bounds__(kSThreads, 1)
     uint16_t* wrun = reinterpret_cast<uint16_t*>(loc + nb1);                               // [kSWarps][nb1]
     __shared__ uint32_t ws[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t items = (int64_t)T * L;
     if (threadIdx.x == 0) {
         for (int i = 0; i < nst; ++i) g_mbar_init(bars + i);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -435,7 +431,6 @@ __global__ void __launch_bounds__(kSThreads, 1)
         if (cc.t >= L) break;
         const int t = cc.t, tile = cc.tile;
         const L1Spec sp0 = spec[t];
-        const int nbits1 = sp0.nbits;
         const int64_t tb = (int64_t)t * n;
         const int cnt = (int)min((int64_t)kG1Tile, n - (int64_t)tile * kG1Tile);
         uint64_t* kr = rk + (size_t)st * kG1Tile;

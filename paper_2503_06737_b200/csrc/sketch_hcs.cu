@@ -61,17 +61,6 @@ size_t hcs_smem_bytes(int S, int M12, int m, int ne, int nst) {
     return (size_t)hcs_tw(S) * 4 + (size_t)S * 2 + (size_t)2 * M12 * 32 * 4 + (size_t)m * 4 + (size_t)ne * 8 + 64;
 }
 
-namespace {
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-}  // namespace
 
 // CPW = S / 16, BPW = M12 / 16 (bins per warp).
 //
