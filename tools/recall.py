@@ -9,7 +9,11 @@ Synthetic stand-in (the paper's datasets are not available): n points in d = 409
 other draws from the same clusters.  Euclidean family only (E2LSH, CS-E2LSH,
 HCS-E2LSH); w = 4 x the mean distance to the k-th true neighbour.
 
-    python tools/recall.py [--n 50000] [--queries 200] [--Ls 1,2,4,8,16,32,50]
+    python tools/recall.py [--n 50000] [--queries 200] [--Ls 1,2,4,8,16,32,50] [--repeats 20]
+
+Each (scheme, L) point is averaged over `repeats` independent hash draws (seeds
+0..repeats-1; the paper averages 20 repetitions); std over repeats is
+reported with the mean.
 """
 import argparse
 import json
@@ -52,6 +56,9 @@ def main():
     ap.add_argument("--w", type=float, default=0.0, help="bucket width; 0 = 4 x mean distance to the k-th neighbour")
     ap.add_argument("--Ls", default="1,2,4,8,16,32,50")
     ap.add_argument("--out", default="")
+    ap.add_argument("--repeats", type=int, default=1)
+    ap.add_argument("--family", default="e2lsh", choices=["e2lsh", "srp"],
+                    help="e2lsh: Euclidean top-k; srp: cosine top-k (CS-SRP, HCS-SRP, SRP)")
     a = ap.parse_args()
     g = torch.Generator(device="cuda").manual_seed(2025)
     C = torch.randn((a.clusters, a.d), device="cuda", generator=g)
@@ -62,41 +69,55 @@ def main():
     Xh, Qh = X.double().cpu().numpy(), Q.double().cpu().numpy()
     xx = (Xh ** 2).sum(1)
     gt, kth = [], []
+    xn = np.sqrt(xx)
     for i in range(a.queries):
-        dd = xx - 2.0 * (Xh @ Qh[i]) + (Qh[i] ** 2).sum()
+        if a.family == "srp":   # cosine similarity, descending (reading C2)
+            dd = -(Xh @ Qh[i]) / np.maximum(xn * np.linalg.norm(Qh[i]), 1e-300)
+        else:
+            dd = xx - 2.0 * (Xh @ Qh[i]) + (Qh[i] ** 2).sum()
         order = np.lexsort((np.arange(a.n), dd))
         gt.append(set(order[: a.k].tolist()))
         kth.append(float(np.sqrt(max(dd[order[a.k - 1]], 0.0))))
-    if a.w <= 0:
+    if a.family == "srp":
+        a.w = 1.0                          # unused by SRP (must be > 0)
+    elif a.w <= 0:
         a.w = 4.0 * float(np.mean(kth))   # E2LSH width ~ a few near-neighbour radii
     rows = []
-    for scheme in ("CS_E2LSH", "HCS_E2LSH", "E2LSH"):
+    schemes = ("CS_SRP", "HCS_SRP", "SRP") if a.family == "srp" else ("CS_E2LSH", "HCS_E2LSH", "E2LSH")
+    for scheme in schemes:
         for L in [int(x) for x in a.Ls.split(",")]:
             m = a.K * L
             kw = {}
             if scheme.startswith("HCS"):
                 kw = dict(mode_d=(16, 16, 16), mode_m=factor3(m))
-            h = pk.LSH(scheme, a.d, m, L, a.K, a.w, 0, **kw)
-            idx = h.build_index(X)
-            torch.cuda.synchronize()
-            for _ in range(2):
-                h.query_knn(idx, X, Q, a.k, max_cand=8192)
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            ids, sc, nc = h.query_knn(idx, X, Q, a.k, max_cand=8192)
-            e1.record()
-            torch.cuda.synchronize()
-            ids = ids.cpu().numpy()
-            rec = float(np.mean([len(gt[i] & set(ids[i][ids[i] >= 0].tolist())) / a.k for i in range(a.queries)]))
-            row = {"scheme": scheme, "L": L, "m": m, "recall_at_k": rec, "query_ms": e0.elapsed_time(e1),
-                   "mean_candidates": float(nc.float().mean().item())}
+            recs, qms, ncs = [], [], []
+            for rep in range(a.repeats):
+                h = pk.LSH(scheme, a.d, m, L, a.K, a.w, rep, **kw)
+                idx = h.build_index(X)
+                torch.cuda.synchronize()
+                for _ in range(2):
+                    h.query_knn(idx, X, Q, a.k, max_cand=8192)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                ids, sc, nc = h.query_knn(idx, X, Q, a.k, max_cand=8192)
+                e1.record()
+                torch.cuda.synchronize()
+                ids = ids.cpu().numpy()
+                recs.append(float(np.mean([len(gt[i] & set(ids[i][ids[i] >= 0].tolist())) / a.k
+                                           for i in range(a.queries)])))
+                qms.append(e0.elapsed_time(e1))
+                ncs.append(float(nc.float().mean().item()))
+                idx.close()
+                h.close()
+            row = {"scheme": scheme, "L": L, "m": m, "recall_at_k": float(np.mean(recs)),
+                   "recall_std": float(np.std(recs)), "repeats": a.repeats, "query_ms": float(np.median(qms)),
+                   "mean_candidates": float(np.mean(ncs))}
             rows.append(row)
             print(json.dumps(row), flush=True)
-            idx.close()
-            h.close()
     res = {"protocol": "PAPER.md:2000-2003 (k=50, K=8 per table, recall vs L), synthetic clustered data",
-           "n": a.n, "d": a.d, "queries": a.queries, "kth_nn_distance": float(np.mean(kth)), "clusters": a.clusters, "sigma": a.sigma, "w": a.w, "rows": rows}
+           "family": a.family,
+           "n": a.n, "d": a.d, "queries": a.queries, "repeats": a.repeats, "kth_nn_distance": float(np.mean(kth)), "clusters": a.clusters, "sigma": a.sigma, "w": a.w, "rows": rows}
     if a.out:
         with open(a.out, "w") as f:
             json.dump(res, f, indent=1)
