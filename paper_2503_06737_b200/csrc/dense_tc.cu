@@ -280,22 +280,43 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 }
 
 // x (fp32) -> [x0 | x1 | x2] bf16, row length 3*d_pad, zero padded (exact split).
-__global__ void split3_kernel(const float* __restrict__ X, int64_t n, int64_t ld, int d, int d_pad,
-                              __nv_bfloat16* __restrict__ A) {
-    const int64_t total = n * (int64_t)d_pad;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = i / d_pad;
-        const int k = (int)(i % d_pad);
-        const float x = k < d ? X[r * ld + k] : 0.f;
-        const __nv_bfloat16 x0 = __float2bfloat16_rn(x);
-        const float r1 = x - __bfloat162float(x0);
-        const __nv_bfloat16 x1 = __float2bfloat16_rn(r1);
-        const float r2 = r1 - __bfloat162float(x1);
-        const __nv_bfloat16 x2 = __float2bfloat16_rn(r2);
-        __nv_bfloat16* row = A + r * (int64_t)(3 * d_pad);
-        row[k] = x0;
-        row[d_pad + k] = x1;
-        row[2 * d_pad + k] = x2;
+// Block per row (grid-stride over rows), thread per 4 consecutive columns: one
+// 128-bit load (when rows are 16-byte aligned) and one 8-byte store per term.
+__device__ __forceinline__ uint32_t pack_bf16x2(__nv_bfloat16 lo, __nv_bfloat16 hi) {
+    return (uint32_t)__bfloat16_as_ushort(lo) | ((uint32_t)__bfloat16_as_ushort(hi) << 16);
+}
+__global__ void __launch_bounds__(256) split3_kernel(const float* __restrict__ X, int64_t n, int64_t ld, int d,
+                                                     int d_pad, int vec_ok, __nv_bfloat16* __restrict__ A) {
+    const int q4 = d_pad >> 2;
+    for (int64_t r = blockIdx.x; r < n; r += gridDim.x) {
+        const float* xr = X + r * ld;
+        uint2* row = reinterpret_cast<uint2*>(A + r * (int64_t)(3 * d_pad));
+        for (int c4 = threadIdx.x; c4 < q4; c4 += blockDim.x) {
+            const int k = 4 * c4;
+            float v[4];
+            if (vec_ok && k + 4 <= d) {
+                const float4 f = __ldcs(reinterpret_cast<const float4*>(xr + k));
+                v[0] = f.x;
+                v[1] = f.y;
+                v[2] = f.z;
+                v[3] = f.w;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) v[j] = k + j < d ? xr[k + j] : 0.f;
+            }
+            __nv_bfloat16 t0[4], t1[4], t2[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                t0[j] = __float2bfloat16_rn(v[j]);
+                const float r1 = v[j] - __bfloat162float(t0[j]);
+                t1[j] = __float2bfloat16_rn(r1);
+                const float r2 = r1 - __bfloat162float(t1[j]);
+                t2[j] = __float2bfloat16_rn(r2);
+            }
+            row[c4] = make_uint2(pack_bf16x2(t0[0], t0[1]), pack_bf16x2(t0[2], t0[3]));
+            row[q4 + c4] = make_uint2(pack_bf16x2(t1[0], t1[1]), pack_bf16x2(t1[2], t1[3]));
+            row[2 * q4 + c4] = make_uint2(pack_bf16x2(t2[0], t2[1]), pack_bf16x2(t2[2], t2[3]));
+        }
     }
 }
 
@@ -388,11 +409,10 @@ cudaError_t launch_dense_tc(const float* X, int64_t n, int64_t ld, int d, const 
         return cudaErrorInvalidValue;
     for (int64_t r0 = 0; r0 < n; r0 += rows_per_batch) {
         const int64_t nb = n - r0 < rows_per_batch ? n - r0 : rows_per_batch;
-        const int64_t total = nb * d_pad;
-        const int threads = 256;
-        const int blocks = (int)((total + threads - 1) / threads < 148 * 64 ? (total + threads - 1) / threads : 148 * 64);
-        split3_kernel<<<blocks, threads, 0, s>>>(X + r0 * ld, nb, ld, d, d_pad,
-                                                 reinterpret_cast<__nv_bfloat16*>(A_scratch));
+        const int vec_ok = ((ld % 4) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0) ? 1 : 0;
+        const int blocks = (int)(nb < 148 * 16 ? nb : 148 * 16);
+        split3_kernel<<<blocks, 256, 0, s>>>(X + r0 * ld, nb, ld, d, d_pad, vec_ok,
+                                             reinterpret_cast<__nv_bfloat16*>(A_scratch));
         count_launch();
         CUtensorMap ma;
         if (!make_map(&ma, A_scratch, (uint64_t)3 * d_pad, (uint64_t)nb, (uint64_t)3 * d_pad * 2, tc::BK, tc::BM))

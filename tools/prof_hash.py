@@ -19,11 +19,12 @@ ap.add_argument("--scheme", default="CS_E2LSH")
 ap.add_argument("--op", default="hash")
 ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--n", type=int, default=0)
+ap.add_argument("--per-table", action="store_true")
 a = ap.parse_args()
 c = synth.CONFIGS[a.config]
 n = a.n or c.n
 kw = dict(mode_d=c.mode_d, mode_m=c.mode_m) if a.scheme.startswith("HCS") else {}
-h = pk.LSH(a.scheme, c.d, c.m, c.L, c.K, c.w, c.hash_seed, **kw)
+h = pk.LSH(a.scheme, c.d, c.m, c.L, c.K, c.w, c.hash_seed, per_table=a.per_table, **kw)
 X = synth.rows(c, 0, n, device="cuda")
 keys = torch.empty((c.L, n), dtype=torch.uint64, device="cuda")
 pk.timing_enable(True)
