@@ -239,18 +239,30 @@ def srp_keys(bits: np.ndarray, L: int, K: int) -> np.ndarray:
     return out
 
 
+# Reading B10: the 64-bit bucket key of one table's K codes is two
+# independent 32-bit polynomial (Horner) hashes of the codes, concatenated and
+# passed through the SplitMix64 finaliser.  Odd multipliers make every Horner
+# step a bijection of the state; fmix64 is a bijection, so two tuples share a key
+# iff both 32-bit polynomials agree.
+FP_A = 0x9E3779B1   # odd 32-bit multipliers of the two lanes
+FP_B = 0x85EBCA77
+MASK32 = 0xFFFFFFFF
+
+
 def fingerprint(words: Sequence[int]) -> int:
     """64-bit key of one table's K codes (reading B10).
 
-    FNV-1a-64 over the K codes taken as 32-bit two's-complement words, then the
-    SplitMix64 finaliser: f = OFFSET; f = (f XOR word) * PRIME mod 2^64 per word;
-    key = fmix64(f).  Integer-only, so any two correct implementations agree.
+    u_k = z_k as a 32-bit two's-complement word;
+    a = sum_k u_k * FP_A^(K-1-k) mod 2^32, b = sum_k u_k * FP_B^(K-1-k) mod 2^32
+    (evaluated by Horner: a <- a*FP_A + u_k from a = 0);
+    key = fmix64(a * 2^32 + b).  Integer-only, so any two correct implementations agree.
     """
-    f = rng.FNV64_OFFSET
+    a = b = 0
     for z in words:
-        f ^= int(z) & 0xFFFFFFFF
-        f = (f * rng.FNV64_PRIME) & rng.MASK64
-    return rng.fmix64(f)
+        u = int(z) & MASK32
+        a = (a * FP_A + u) & MASK32
+        b = (b * FP_B + u) & MASK32
+    return rng.fmix64((a << 32) | b)
 
 
 def _fmix64_np(z: np.ndarray) -> np.ndarray:
@@ -265,13 +277,16 @@ def e2lsh_keys(codes: np.ndarray, L: int, K: int) -> np.ndarray:
     """fingerprint() of every (point, table), elementwise over points (uint64 [L][n])."""
     n = codes.shape[0]
     out = np.zeros((L, n), dtype=np.uint64)
-    words = (np.asarray(codes, dtype=np.int64) & 0xFFFFFFFF).astype(np.uint64)
+    words = (np.asarray(codes, dtype=np.int64) & MASK32).astype(np.uint64)
+    m32 = np.uint64(MASK32)
     with np.errstate(over="ignore"):
         for t in range(L):
-            f = np.full(n, rng.FNV64_OFFSET, dtype=np.uint64)
+            a = np.zeros(n, dtype=np.uint64)
+            b = np.zeros(n, dtype=np.uint64)
             for k in range(K):
-                f = (f ^ words[:, t * K + k]) * np.uint64(rng.FNV64_PRIME)
-            out[t] = _fmix64_np(f)
+                a = (a * np.uint64(FP_A) + words[:, t * K + k]) & m32
+                b = (b * np.uint64(FP_B) + words[:, t * K + k]) & m32
+            out[t] = _fmix64_np((a << np.uint64(32)) | b)
     return out
 
 
@@ -331,7 +346,7 @@ def group_by_tuple(codes_t: np.ndarray) -> Dict[tuple, List[int]]:
 
 
 def fingerprint_merges(codes: np.ndarray, keys: np.ndarray, L: int, K: int) -> int:
-    """Number of (table, key) pairs whose bucket mixes different exact K-tuples."""
+    """Rows whose exact K-tuple differs from the first tuple filed under the same (table, key)."""
     merges = 0
     for t in range(L):
         seen: Dict[int, tuple] = {}

@@ -212,18 +212,84 @@ def test_work_is_o_d_for_sketches_and_o_md_for_dense():
         assert lsh.projection_op_count(p, lsh.make_tables(p), x) == 64 * m
 
 
-def test_fingerprint_components():
-    # FNV-1a over 32-bit words < 256 equals byte-wise FNV-1a over those bytes,
-    # and the finaliser is SplitMix64's output function (pinned by its vectors).
-    words = [3, 0, 255, 17, 42]
-    f = rng.FNV64_OFFSET
-    for wv in words:
-        f ^= wv
-        f = (f * rng.FNV64_PRIME) & rng.MASK64
-    assert f == rng.fnv1a64(bytes(words))
-    assert lsh.fingerprint(words) == rng.fmix64(rng.fnv1a64(bytes(words)))
-    # negative codes use two's complement words
-    assert lsh.fingerprint([-1]) == rng.fmix64(((rng.FNV64_OFFSET ^ 0xFFFFFFFF) * rng.FNV64_PRIME) & rng.MASK64)
+def test_fingerprint_special_cases():
+    # Reading B10 reduces to the SplitMix64 finaliser (pinned by its published vectors)
+    # on inputs whose two polynomial lanes are known without evaluating the lanes:
+    # all-zero codes give lanes (0, 0); a single code u gives lanes (u, u).
+    assert lsh.fingerprint([0] * 16) == rng.fmix64(0) == 0
+    assert lsh.fingerprint([1]) == rng.fmix64((1 << 32) | 1)
+    assert lsh.fingerprint([-1]) == rng.fmix64(0xFFFFFFFFFFFFFFFF)     # two's complement word
+    assert lsh.fingerprint([-(1 << 31)]) == rng.fmix64(0x8000000080000000)
+    # leading zero codes leave both Horner lanes at 0 (the polynomial is in u_{K-1} last)
+    assert lsh.fingerprint([0, 0, 0, 5]) == lsh.fingerprint([5])
+    # a code in front is multiplied by the lane's multiplier once per later code
+    A, B = lsh.FP_A, lsh.FP_B
+    assert lsh.fingerprint([1, 0]) == rng.fmix64((A << 32) | B)
+    assert lsh.fingerprint([1, 0, 0]) == rng.fmix64(((A * A % 2 ** 32) << 32) | (B * B % 2 ** 32))
+
+
+def _lane_values(mult: int, K: int, radius: int, lo: int, hi: int) -> np.ndarray:
+    """sum_{k in [lo,hi)} delta_k * mult^(K-1-k) mod 2^32 over every delta in [-r, r]^(hi-lo)."""
+    out = np.zeros(1, dtype=np.int64)
+    for k in range(lo, hi):
+        c = pow(mult, K - 1 - k, 1 << 32)
+        out = np.concatenate([out + j * c for j in range(-radius, radius + 1)])
+    return out % (1 << 32)
+
+
+@pytest.mark.parametrize("K", [8, 16])
+def test_fingerprint_separates_nearby_code_tuples(K):
+    """No two K-code tuples that differ by at most 2 in every coordinate share a key.
+
+    Near neighbours of an E2LSH code differ by small amounts in a few coordinates
+    (adjacent bins), so those are the merges that would matter.  Key equality
+    of z and z' = both lanes agree = P_A(z - z') = P_B(z - z') = 0 mod 2^32 (fmix64 is
+    a bijection); checked exhaustively over all 5^K differences by meet in the middle.
+    """
+    M = 1 << 32
+    h = K // 2
+    la = _lane_values(lsh.FP_A, K, 2, 0, h)
+    ra = (-_lane_values(lsh.FP_A, K, 2, h, K)) % M
+    lb = _lane_values(lsh.FP_B, K, 2, 0, h)
+    rb = _lane_values(lsh.FP_B, K, 2, h, K)
+    order = np.argsort(ra, kind="stable")
+    rs = ra[order]
+    p0 = np.searchsorted(rs, la, side="left")
+    p1 = np.searchsorted(rs, la, side="right")
+    both = 0
+    for i in np.nonzero(p1 > p0)[0]:
+        for q in range(p0[i], p1[i]):
+            if (lb[i] + rb[order[q]]) % M == 0:
+                both += 1
+    assert both == 1   # only the zero difference (z == z')
+
+
+def test_fingerprint_separates_two_coordinate_changes():
+    """No two tuples differing in exactly two coordinates by up to 4096 each share a key
+    (d_i A^p + d_j A^q = 0 mod 2^32 would need d_i = -d_j A^(q-p))."""
+    M = 1 << 32
+    R = 4096
+    d = np.arange(-R, R + 1, dtype=np.int64)
+    d = d[d != 0]
+    for mult in (lsh.FP_A, lsh.FP_B):
+        for r in range(1, 16):
+            v = (d * pow(mult, r, M)) % M
+            v = np.where(v >= M // 2, v - M, v)
+            assert not np.any(np.abs(v) <= R), (hex(mult), r)
+
+
+def test_fingerprint_merges_counts_forced_collisions():
+    """fingerprint_merges counts the rows whose K-tuple differs from the first tuple filed
+    under the same (table, key): forced collisions (keys chosen equal for different codes)
+    must be counted, equal tuples under one key must not."""
+    codes = np.array([[1, 2, 0, 0], [1, 2, 0, 1], [3, 4, 0, 0], [1, 2, 5, 5], [3, 4, 5, 5]])
+    # table 0 = columns 0..1, table 1 = columns 2..3
+    keys = np.array([[7, 7, 9, 7, 7],          # t0: rows 0,1,3 are (1,2) under 7: fine; row 4 (3,4) under 7: merge
+                     [1, 2, 1, 3, 3]], dtype=np.uint64)   # t1: row 2 (0,0) under 1 with row 0: fine; row 4 (5,5) = row 3: fine
+    assert lsh.fingerprint_merges(codes, keys, 2, 2) == 1
+    keys[1, 1] = 1                               # (0,1) under the key of (0,0): a second merge
+    assert lsh.fingerprint_merges(codes, keys, 2, 2) == 2
+    assert lsh.fingerprint_merges(codes, lsh.e2lsh_keys(codes, 2, 2), 2, 2) == 0
 
 
 def test_srp_key_packing():
