@@ -24,7 +24,8 @@
  *     when prod d_k > d (B6, B7).
  *   - A table's bucket key: SRP = the K bits packed little-endian (bit k of the key =
  *     code coordinate t*K+k), exact; E2LSH = 64-bit fingerprint of the K int32 codes
- *     (FNV-1a-64 over 32-bit two's-complement words, then the SplitMix64 finaliser) (B10).
+ *     u_k (two's-complement words): lanes a = sum u_k A^(K-1-k), b = sum u_k B^(K-1-k)
+ *     mod 2^32 (A = 0x9E3779B1, B = 0x85EBCA77), key = SplitMix64-finaliser(a:b) (B10).
  *   - Inside a table, buckets are ordered by ascending unsigned key and ids ascend
  *     inside a bucket (B11).
  *   - Random parameters derive from `seed` exactly as DESIGN.md R1-R4 state
@@ -39,7 +40,9 @@
  *     default stream) passed as void* so this header needs no CUDA include.
  *   - Device calls are stream-ordered and asynchronous (no host synchronisation)
  *     unless stated otherwise.  Handles and built indexes are immutable and may be
- *     used concurrently from several streams.
+ *     used concurrently from several streams: every index consumer (queries, counts)
+ *     first makes its stream wait for the index's build, and lsh_index_destroy orders
+ *     the release of the index memory after the last use on every such stream.
  *   - X is row-major fp32 [n][ld], ld >= d (elements), rows contiguous.
  *   - Errors: LSH_EINVAL invalid parameters (w <= 0, m != L*K, prod mode_m != m,
  *     prod mode_d < d, K > 64 for SRP, m > 2^20, d > 2^27, N outside 1..8);
@@ -134,7 +137,7 @@ lsh_status lsh_hash(const lsh_handle* h, const float* X, int64_t n, int64_t ld,
 /* ---- index (§8(a) rows a-5, a-7) ---------------------------------------- */
 
 /* Hash X and group the n points into the buckets of every table; point i gets the
- * global id (id_base + i) (uint32; id_base + n <= 2^32).  n == 0 gives an empty
+ * global id (id_base + i) (uint32; id_base + n <= 2^32 - 1: 0xffffffff is reserved).  n == 0 gives an empty
  * index.  Asynchronous: *out is valid immediately, its contents after `stream`
  * reaches this point. */
 lsh_status lsh_build_index(const lsh_handle* h, const float* X, int64_t n, int64_t ld,
@@ -227,8 +230,9 @@ uint64_t lsh_launch_count(void);
 /* Per-kernel device time: when enabled, every internal launch on a handle is
  * bracketed by CUDA events on its stream and accumulated by kernel name. */
 void lsh_timing_enable(int32_t on);
-/* Names: "sketch", "dense_gemm", "keys_from_proj", "radix_upsweep", "radix_downsweep",
- * "radix_scan", "segsort", "rle", "lookup", "counts".  Synchronises the device.
+/* Names: "sketch", "sketch_query", "dense_gemm", "dense_gemm_query", "keys_from_proj",
+ * "group_hist", "group_scan", "group_scatter", "group_sort", "lookup", "knn", "counts",
+ * "global_offsets".  Synchronises the device.
  * Returns accumulated milliseconds and launch count since the last reset. */
 lsh_status lsh_timing_get(const char* name, double* ms, int64_t* launches);
 void lsh_timing_reset(void);

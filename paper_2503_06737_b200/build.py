@@ -15,7 +15,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "liblsh_b200.so")
-SOURCES = ["api.cu", "sketch.cu", "sketch_chunked.cu", "sketch_hcs.cu", "group.cu", "dense.cu", "dense_tc.cu", "knn.cu"]
+SOURCES = ["api.cu", "sketch.cu", "sketch_fast.cu", "sketch_chunked.cu", "sketch_hcs.cu", "group.cu", "dense_tc.cu", "knn.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -36,16 +36,21 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    if not force and not _stale():
+def build(verbose: bool = False, force: bool = False, variant: str = "") -> str:
+    """variant "prof": diagnostic library liblsh_b200_prof.so (-DLSHB_PROF: per-phase
+    clock counters); never loaded by the product path."""
+    target = OUT if not variant else OUT.replace(".so", f"_{variant}.so")
+    if not variant and not force and not _stale():
         return OUT
     objs = []
-    tmp = os.path.join(HERE, "build")
+    tmp = os.path.join(HERE, "build" + (f"_{variant}" if variant else ""))
     os.makedirs(tmp, exist_ok=True)
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
                     "-I" + os.path.join(HERE, "..", "include")]
     if verbose:
         flags += ["-Xptxas", "-v"]
+    if variant == "prof":
+        flags += ["-DLSHB_PROF"]
     procs = []
     for src in SOURCES:
         obj = os.path.join(tmp, src.replace(".cu", ".o"))
@@ -58,14 +63,15 @@ def build(verbose: bool = False, force: bool = False) -> str:
             sys.stderr.write(out.decode(errors="replace"))
         if pr.returncode != 0:
             raise RuntimeError("nvcc failed: " + " ".join(cmd))
-    link = [nvcc()] + ARCH + ["-shared", "-cudart", "static", "-o", OUT + ".tmp"] + objs + ["-lpthread"]
+    link = [nvcc()] + ARCH + ["-shared", "-cudart", "static", "-o", target + ".tmp"] + objs + ["-lpthread"]
     r = subprocess.run(link, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
     if r.returncode != 0:
         sys.stderr.write(r.stdout.decode(errors="replace"))
         raise RuntimeError("link failed")
-    os.replace(OUT + ".tmp", OUT)
-    return OUT
+    os.replace(target + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":
-    print(build(verbose="--verbose" in sys.argv, force=True))
+    v = sys.argv[sys.argv.index("--variant") + 1] if "--variant" in sys.argv else ""
+    print(build(verbose="--verbose" in sys.argv, force=True, variant=v))

@@ -3,7 +3,7 @@
 // Validates the problem statement, draws the random parameters on the host
 // (params.hpp, R1-R4), plans the device execution (per-chunk bin lists
 // for the sketch kernel), owns device buffers of handles and indexes, and
-// launches the kernels of sketch.cu / dense.cu / group.cu on the caller's stream.
+// launches the kernels of sketch*.cu / dense_tc.cu / group.cu / knn.cu on the caller's stream.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -158,6 +158,9 @@ static lsh_status validate(const lsh_params* p) {
     if (!(p->w > 0.0f) || !std::isfinite(p->w)) return LSH_EINVAL;
     if (!is_e2lsh(p->scheme) && p->K > 64) return LSH_EINVAL;
     if (p->flags & ~LSH_FLAG_PER_TABLE) return LSH_EINVAL;
+    // dense R / per-table sign matrix: m*d bf16 on the host and the device (<= 32 GiB)
+    if ((is_dense(p->scheme) || (p->flags & LSH_FLAG_PER_TABLE)) && (int64_t)p->m * p->d > (1ll << 34))
+        return LSH_EINVAL;
     if ((p->flags & LSH_FLAG_PER_TABLE) && !(p->scheme == LSH_CS_E2LSH || p->scheme == LSH_CS_SRP))
         return LSH_EUNSUPPORTED;
     if (is_hcs(p->scheme)) {
@@ -318,7 +321,29 @@ struct lsh_index {
     void* mem = nullptr;
     cudaEvent_t done = nullptr;
     cudaStream_t stream = nullptr;  // build stream: memory is freed stream-ordered on it
+    // Consumers on other streams (queries, counts): each waits on `done` before reading,
+    // and records a last-use event here, so destroy can order the stream-ordered free
+    // after every reader without a host synchronisation.
+    mutable std::mutex use_mu;
+    mutable std::vector<std::pair<cudaStream_t, cudaEvent_t>> uses;
 };
+
+// Start of an index consumer on stream s: the build must be complete.
+static cudaError_t index_acquire(const lsh_index* I, cudaStream_t s) { return cudaStreamWaitEvent(s, I->done, 0); }
+// End of an index consumer on stream s: remember the stream's last use.
+static void index_release(const lsh_index* I, cudaStream_t s) {
+    if (s == I->stream) return;   // the free is stream-ordered on the build stream already
+    std::lock_guard<std::mutex> g(I->use_mu);
+    for (auto& u : I->uses)
+        if (u.first == s) {
+            cudaEventRecord(u.second, s);
+            return;
+        }
+    cudaEvent_t e;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return;
+    cudaEventRecord(e, s);
+    I->uses.emplace_back(s, e);
+}
 
 // Chunked plan (large d and/or m): tables in groups whose partial sums fit in
 // shared memory; per group, the coordinates whose bin lies in the group (ascending),
@@ -410,9 +435,10 @@ static lsh_status build_chunked_plan(lsh_handle* H, const std::vector<int32_t>& 
     CK(cudaMalloc(&H->d_cplan_mem, total));
     char* base = (char*)H->d_cplan_mem;
     size_t o = 0;
+    cudaError_t perr = cudaSuccess;
     auto put = [&](const void* src, size_t b) {
         char* dst = base + o;
-        if (b) cudaMemcpy(dst, src, b, cudaMemcpyHostToDevice);
+        if (b && perr == cudaSuccess) perr = cudaMemcpy(dst, src, b, cudaMemcpyHostToDevice);
         o += al(b);
         return (void*)dst;
     };
@@ -431,6 +457,7 @@ static lsh_status build_chunked_plan(lsh_handle* H, const std::vector<int32_t>& 
     cp.sgn = (const uint32_t*)put(sgnb.data(), b_sg);
     cp.bp = (const uint32_t*)put(bp.data(), b_bp);
     cp.cnt = (const uint8_t*)put(cnt.data(), b_cn);
+    CK(perr);
     H->cplan = cp;
     H->chunked = true;
     return LSH_OK;
@@ -562,9 +589,9 @@ static lsh_status build_plan(lsh_handle* H) {
     for (int l = 0; l < m; ++l) bin_ptr[l + 1] += bin_ptr[l];
     {
         std::vector<uint32_t> cur(bin_ptr.begin(), bin_ptr.end() - 1);
-        for (int j = 0; j < d; ++j) ent[cur[bin[j]]++] = (uint16_t)((j >> 2) * 129 + (j & 3) * 32);
+        for (int j = 0; j < d; ++j) ent[cur[bin[j]]++] = (uint16_t)((j >> 2) * kSketchColWords + (j & 3) * 32);
     }
-    const uint32_t ZW = (uint32_t)(Q / 4) * 129u;
+    const uint32_t ZW = (uint32_t)(Q / 4) * (uint32_t)kSketchColWords;
     int max_cnt = 0;
     std::vector<uint32_t> pairs(2 * (size_t)m), bigmask(p->L, 0);
     for (int l = 0; l < m; ++l) {
@@ -634,7 +661,11 @@ extern "C" lsh_status lsh_create(const lsh_params* p, lsh_handle** out) {
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         }
     }
-    draw(p, H->host, true);
+    try {
+        draw(p, H->host, true);
+    } catch (...) {
+        return fail(LSH_ENOMEM);
+    }
     H->key_width = is_e2lsh(p->scheme) ? 64 : p->K;
     const int m = p->m;
     // offsets folded with w: c_off[l] = b_l / w; c_scale = sqrt(m)/w (CS/HCS) or 1/w (dense)
@@ -649,11 +680,12 @@ extern "C" lsh_status lsh_create(const lsh_params* p, lsh_handle** out) {
     if ((e = cudaMemcpy(H->d_coff, coff.data(), sizeof(float) * m, cudaMemcpyHostToDevice)) != cudaSuccess)
         return fail(cuda_fail(e, "memcpy"));
     if ((e = cudaMalloc(&H->d_flags, sizeof(int))) != cudaSuccess) return fail(cuda_fail(e, "malloc"));
-    cudaMemset(H->d_flags, 0, sizeof(int));
+    if ((e = cudaMemset(H->d_flags, 0, sizeof(int))) != cudaSuccess) return fail(cuda_fail(e, "memset"));
     H->disc.c_off = H->d_coff;
     H->disc.flags = H->d_flags;
     if ((e = cudaMalloc(&H->d_b, sizeof(float) * m)) != cudaSuccess) return fail(cuda_fail(e, "malloc"));
-    cudaMemcpy(H->d_b, H->host.b.data(), sizeof(float) * m, cudaMemcpyHostToDevice);
+    if ((e = cudaMemcpy(H->d_b, H->host.b.data(), sizeof(float) * m, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return fail(cuda_fail(e, "memcpy b"));
     if (uses_R(p)) {
         const size_t bytes = sizeof(uint16_t) * H->host.R.size();
         if ((e = cudaMalloc(&H->d_R, bytes)) != cudaSuccess) return fail(cuda_fail(e, "malloc R"));
@@ -662,7 +694,7 @@ extern "C" lsh_status lsh_create(const lsh_params* p, lsh_handle** out) {
         H->d_pad = (int)((p->d + 63) / 64 * 64);
         const size_t pbytes = sizeof(uint16_t) * (size_t)m * H->d_pad;
         if ((e = cudaMalloc(&H->d_Rpad, pbytes)) != cudaSuccess) return fail(cuda_fail(e, "malloc Rpad"));
-        cudaMemset(H->d_Rpad, 0, pbytes);
+        if ((e = cudaMemset(H->d_Rpad, 0, pbytes)) != cudaSuccess) return fail(cuda_fail(e, "memset Rpad"));
         if ((e = cudaMemcpy2D(H->d_Rpad, sizeof(uint16_t) * H->d_pad, H->d_R, sizeof(uint16_t) * p->d,
                               sizeof(uint16_t) * p->d, m, cudaMemcpyDeviceToDevice)) != cudaSuccess)
             return fail(cuda_fail(e, "pad R"));
@@ -674,11 +706,16 @@ extern "C" lsh_status lsh_create(const lsh_params* p, lsh_handle** out) {
             H->d_h.push_back(dh);
             if ((e = cudaMalloc(&ds, bytes)) != cudaSuccess) return fail(cuda_fail(e, "malloc s"));
             H->d_s.push_back(ds);
-            cudaMemcpy(dh, H->host.h[k].data(), bytes, cudaMemcpyHostToDevice);
-            cudaMemcpy(ds, H->host.s[k].data(), bytes, cudaMemcpyHostToDevice);
+            if ((e = cudaMemcpy(dh, H->host.h[k].data(), bytes, cudaMemcpyHostToDevice)) != cudaSuccess ||
+                (e = cudaMemcpy(ds, H->host.s[k].data(), bytes, cudaMemcpyHostToDevice)) != cudaSuccess)
+                return fail(cuda_fail(e, "memcpy h/s"));
         }
-        st = build_plan(H);
-        if (st == LSH_OK) st = build_hcs_plan(H);
+        try {
+            st = build_plan(H);
+            if (st == LSH_OK) st = build_hcs_plan(H);
+        } catch (...) {
+            st = LSH_ENOMEM;
+        }
         if (st != LSH_OK) return fail(st);
     }
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail(cuda_fail(e, "create sync"));
@@ -713,10 +750,9 @@ static lsh_status hash_impl(const lsh_handle* H, const float* X, int64_t n, int6
     if (out.bits && is_e2lsh(p.scheme)) out.bits = nullptr;
     if (n == 0) return LSH_OK;
     if (uses_R(&p)) {
-        static const bool simt = getenv("LSH_DENSE_SIMT") && getenv("LSH_DENSE_SIMT")[0] == '1';
         static const bool unfused = getenv("LSH_DENSE_UNFUSED") && getenv("LSH_DENSE_UNFUSED")[0] == '1';
         cudaError_t e;
-        if (!simt && !unfused && out.keys && !out.codes && !out.bits && !out.proj &&
+        if (!unfused && out.keys && !out.codes && !out.bits && !out.proj &&
             dense_tc_fused_keys_ok(p.m, p.K)) {
             // keys straight from the accumulators (fused epilogue): no [n][m] projection in HBM
             const int64_t rows = std::min<int64_t>(n, (int64_t)dense_tc_rows_per_batch(H->d_pad));
@@ -733,12 +769,7 @@ static lsh_status hash_impl(const lsh_handle* H, const float* X, int64_t n, int6
         }
         float* Y = out.proj;
         if (!Y) CK(cudaMallocAsync((void**)&Y, sizeof(float) * (size_t)n * p.m, s));
-        if (simt) {  // CUDA-core cross-check kernel (tests only)
-            timing_begin("dense_gemm_simt", s);
-            e = launch_dense_gemm_f32(X, n, ld, H->d_R, p.m, (int)p.d, Y, s);
-            count_launch();
-            timing_end("dense_gemm_simt", s);
-        } else {
+        {
             const int64_t rows = std::min<int64_t>(n, (int64_t)dense_tc_rows_per_batch(H->d_pad));
             uint16_t* A = nullptr;
             CK(cudaMallocAsync((void**)&A, sizeof(uint16_t) * (size_t)rows * 3 * H->d_pad, s));
@@ -826,12 +857,12 @@ static lsh_status group_impl(const lsh_handle* H, const uint64_t* keys, uint64_t
     const size_t b_hist = sizeof(uint32_t) * (size_t)L * std::max<size_t>(group_hist_words(n, H->key_width), 1);
     const size_t b_tot = sizeof(uint32_t) * (size_t)L * nb1;
     const size_t b_bs = sizeof(uint32_t) * (size_t)L * (nb1 + 1);
-    const size_t b_st = sizeof(unsigned long long) * (size_t)L * (size_t)std::max(group_chunks(n), 1);
+    const size_t b_st = sizeof(unsigned long long) * (size_t)L * std::max<size_t>(nb1, (size_t)group_rle_chunks(n));
     const bool own_perm = (keys_scratch == nullptr);
     const size_t b_perm = own_perm ? b_keys : 0;
     const size_t b_vm = sizeof(unsigned long long) * 2 * (size_t)L;
     const size_t b_spec = group_spec_bytes() * 2 * (size_t)L;
-    const size_t b_cb = sizeof(uint32_t) * (size_t)L * ((size_t)std::max(group_chunks(n), 1) + 1);
+    const size_t b_cb = sizeof(uint32_t) * ((size_t)L * nb1 + 1);
     void* mem = nullptr;
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
     const size_t total = al(b_keys) + al(b_ids) + al(b_hist) + al(b_tot) + al(b_bs) + al(b_st) + al(b_perm) + al(b_vm) +
@@ -853,7 +884,8 @@ static lsh_status group_impl(const lsh_handle* H, const uint64_t* keys, uint64_t
         sc.perm = own_perm ? (uint32_t*)take(b_perm) : (uint32_t*)keys_scratch;
         sc.vmask = (unsigned long long*)take(b_vm);
         sc.spec = take(b_spec);
-        sc.chunkbin = (uint32_t*)take(b_cb);
+        sc.bigcount = (uint32_t*)take(b_cb);
+        sc.biglist = sc.bigcount + 1;
     }
     sc.num_sms = H->num_sms;
     cudaError_t e = launch_group(keys, n, L, (uint32_t)id_base, H->key_width, sc, I->dev, H->d_flags, s);
@@ -866,7 +898,7 @@ static lsh_status group_impl(const lsh_handle* H, const uint64_t* keys, uint64_t
 extern "C" lsh_status lsh_group_keys(const lsh_handle* h, const uint64_t* keys, int64_t n, int64_t id_base,
                                      lsh_index** out, void* stream) {
     if (!h || !out) return LSH_ESTATE;
-    if (n < 0 || id_base < 0 || id_base + n > (1ll << 32)) return LSH_EDIM;
+    if (n < 0 || id_base < 0 || id_base + n > (1ll << 32) - 1) return LSH_EDIM;
     CK(cudaSetDevice(h->device));
     cudaStream_t s = (cudaStream_t)stream;
     lsh_index* I = nullptr;
@@ -885,7 +917,7 @@ extern "C" lsh_status lsh_group_keys(const lsh_handle* h, const uint64_t* keys, 
 extern "C" lsh_status lsh_build_index(const lsh_handle* h, const float* X, int64_t n, int64_t ld, int64_t id_base,
                                       lsh_index** out, void* stream) {
     if (!h || !out) return LSH_ESTATE;
-    if (n < 0 || ld < h->p.d || id_base < 0 || id_base + n > (1ll << 32)) return LSH_EDIM;
+    if (n < 0 || ld < h->p.d || id_base < 0 || id_base + n > (1ll << 32) - 1) return LSH_EDIM;
     if (n > 0 && !X) return LSH_EDIM;
     CK(cudaSetDevice(h->device));
     cudaStream_t s = (cudaStream_t)stream;
@@ -931,7 +963,16 @@ extern "C" int64_t lsh_index_size(const lsh_index* idx) { return idx ? idx->n : 
 
 extern "C" void lsh_index_destroy(lsh_index* idx) {
     if (!idx) return;
-    if (idx->done) cudaEventSynchronize(idx->done);
+    cudaSetDevice(idx->h->device);
+    {
+        // the stream-ordered free runs after every recorded reader on other streams
+        std::lock_guard<std::mutex> g(idx->use_mu);
+        for (auto& u : idx->uses) {
+            cudaStreamWaitEvent(idx->stream, u.second, 0);
+            cudaEventDestroy(u.second);
+        }
+        idx->uses.clear();
+    }
     if (idx->mem) cudaFreeAsync(idx->mem, idx->stream);
     if (idx->done) cudaEventDestroy(idx->done);
     delete idx;
@@ -949,11 +990,13 @@ extern "C" lsh_status lsh_query_buckets(const lsh_handle* h, const lsh_index* id
     CK(cudaMallocAsync((void**)&qk, sizeof(uint64_t) * (size_t)h->p.L * nq, s));
     lsh_status st = hash_impl(h, Q, nq, ld, HashOut{qk, nullptr, nullptr, nullptr}, s, "sketch_query");
     if (st == LSH_OK) {
+        CK(index_acquire(idx, s));
         timing_begin("lookup", s);
         cudaError_t e = launch_lookup(qk, nq, h->p.L, idx->n, idx->dev, begin, end, s);
         count_launch();
         timing_end("lookup", s);
         if (e != cudaSuccess) st = cuda_fail(e, "lookup");
+        index_release(idx, s);
     }
     cudaFreeAsync(qk, s);
     return st;
@@ -974,6 +1017,7 @@ extern "C" lsh_status lsh_query_knn(const lsh_handle* h, const lsh_index* idx, c
     CK(cudaMallocAsync((void**)&be, sizeof(int64_t) * 2 * (size_t)nq * L, s));
     lsh_status st = lsh_query_buckets(h, idx, Q, nq, ldq, be, be + (size_t)nq * L, stream);
     if (st == LSH_OK) {
+        CK(index_acquire(idx, s));
         timing_begin("knn", s);
         cudaError_t e = launch_knn(idx->dev, idx->n, L, (uint32_t)idx->id_base, be, be + (size_t)nq * L, X, ldx,
                                    (int)h->p.d, Q, ldq, nq, k, max_cand, is_e2lsh(h->p.scheme) ? 0 : 1, out_ids,
@@ -981,6 +1025,7 @@ extern "C" lsh_status lsh_query_knn(const lsh_handle* h, const lsh_index* idx, c
         count_launch();
         timing_end("knn", s);
         if (e != cudaSuccess) st = cuda_fail(e, "knn");
+        index_release(idx, s);
     }
     cudaFreeAsync(be, s);
     return st;
@@ -991,10 +1036,12 @@ extern "C" lsh_status lsh_index_counts(const lsh_index* idx, int32_t B, uint32_t
     if (B < 1 || B > 20 || !counts) return LSH_EDIM;
     CK(cudaSetDevice(idx->h->device));
     cudaStream_t s = (cudaStream_t)stream;
+    CK(index_acquire(idx, s));
     timing_begin("counts", s);
     cudaError_t e = launch_counts(idx->dev, idx->n, idx->L, idx->h->key_width, B, counts, s);
     count_launch();
     timing_end("counts", s);
+    index_release(idx, s);
     if (e != cudaSuccess) return cuda_fail(e, "counts");
     return LSH_OK;
 }
@@ -1069,9 +1116,13 @@ extern "C" lsh_status lsh_export_host(const lsh_params* p, int32_t what, int32_t
                                       size_t* bytes) {
     lsh_status st = validate(p);
     if (st != LSH_OK) return st;
-    HostTables t;
-    draw(p, t, what == LSH_EXPORT_GAUSSIAN);
-    return export_from(p, t, what, mode, host_buf, bytes);
+    try {
+        HostTables t;
+        draw(p, t, what == LSH_EXPORT_GAUSSIAN);
+        return export_from(p, t, what, mode, host_buf, bytes);
+    } catch (...) {
+        return LSH_ENOMEM;
+    }
 }
 
 extern "C" lsh_status lsh_get_params(const lsh_handle* h, int32_t what, int32_t mode, void* host_buf,

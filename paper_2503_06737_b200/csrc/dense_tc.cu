@@ -233,14 +233,14 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                         if (l0 >= m) break;
                         uint64_t f;
                         if (ke.dz.e2lsh) {
-                            f = LSHB_FNV_OFFSET;
+                            FpKey fk;
 #pragma unroll
                             for (int kk = 0; kk < KT; ++kk) {
                                 const float qv = fmaf(__uint_as_float(v[tb * KT + kk]), ke.dz.c_scale,
                                                       __ldg(ke.dz.c_off + l0 + kk));
-                                f = (f ^ (uint64_t)(uint32_t)floor_code(qv, ke.dz.flags)) * LSHB_FNV_PRIME;
+                                fk.add((uint32_t)floor_code(qv, ke.dz.flags));
                             }
-                            f = fmix64_dev(f);
+                            f = fk.key();
                         } else {
                             f = 0;
 #pragma unroll

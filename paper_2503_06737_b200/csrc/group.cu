@@ -36,10 +36,8 @@ constexpr int kG1Tile = 8192;                   // items per L1 tile
 constexpr int kG1Threads = 256;
 constexpr int kG2Threads = 512;
 constexpr int kG2Warps = kG2Threads / 32;       // 16
-constexpr int kG2Cap = 4096;                    // bin items sorted in shared memory
-constexpr int kG2Span = kG2Cap / 2;            // L2 chunk: bins starting inside a span of this many items
-constexpr int kG2Seg = 64;                      // longest equal-prefix segment finished by O(s) ranks
-constexpr int kG2Long = kG2Cap / kG2Seg;        // long-segment list capacity
+constexpr int kG2Cap = 4096;                    // run-length-encoding chunk (narrow keys)
+constexpr int kG2BinCap = 1280;                 // largest L1 bin sorted in shared memory (g2a)
 
 size_t group_tiles(int64_t n) { return (size_t)((n + kG1Tile - 1) / kG1Tile); }
 
@@ -51,7 +49,7 @@ bool group_is_lsd(int W) { return W <= 22; }
 int group_l1_bits(int64_t n, int W) {
     if (group_is_lsd(W)) return (W + 1) / 2;
     int b = 1;
-    while (b < 11 && ((n + (1ll << b) - 1) >> b) > kG2Span / 2) ++b;
+    while (b < 11 && ((n + (1ll << b) - 1) >> b) > 1024) ++b;   // bins of <= 1024 on average (cap 1280)
     return b < W ? b : W;
 }
 
@@ -286,34 +284,24 @@ __global__ void g1_scan(uint32_t* __restrict__ hist, int T, int L, int nb1, uint
     tot[(int64_t)t * nb1 + b] = run;
 }
 
-// One block per table: bin starts = exclusive scan of the bin totals, and (MSD
-// path) the L2 chunk edges: chunkbin[c] = first bin whose start is >= c*span.
+// One block per table: bin starts = exclusive scan of the bin totals; with a big-bin
+// list (wide keys), every bin larger than kG2BinCap is appended as t * nb1 + bin.
 __global__ void __launch_bounds__(1024) g1_binstart(const uint32_t* __restrict__ tot, int nb1, int64_t n,
-                                                    uint32_t* __restrict__ binstart, int span, int nchunks,
-                                                    uint32_t* __restrict__ chunkbin) {
+                                                    uint32_t* __restrict__ binstart, uint32_t* __restrict__ biglist,
+                                                    uint32_t* __restrict__ bigcount) {
     __shared__ uint32_t ws[32];
-    __shared__ uint32_t sbs[2049];
     const int t = blockIdx.x;
     const int b0 = 2 * threadIdx.x, b1 = b0 + 1;
     const uint32_t v0 = b0 < nb1 ? tot[(int64_t)t * nb1 + b0] : 0u;
     const uint32_t v1 = b1 < nb1 ? tot[(int64_t)t * nb1 + b1] : 0u;
     const uint32_t e = block_excl_scan<1024>(v0 + v1, ws, nullptr);
     uint32_t* bs = binstart + (int64_t)t * (nb1 + 1);
-    if (b0 < nb1) sbs[b0] = bs[b0] = e;
-    if (b1 < nb1) sbs[b1] = bs[b1] = e + v0;
-    if (threadIdx.x == 0) sbs[nb1] = bs[nb1] = (uint32_t)n;
-    if (!chunkbin) return;
-    __syncthreads();
-    uint32_t* cb = chunkbin + (int64_t)t * (nchunks + 1);
-    for (int b = threadIdx.x; b <= nb1; b += blockDim.x) {
-        // chunks c with bs[b-1] < c*span <= bs[b] start at bin b (b == nb1: past the end)
-        const int64_t prev = b ? (int64_t)sbs[b - 1] : -1;
-        const int64_t cur = sbs[b];
-        const int64_t c0 = prev < 0 ? 0 : prev / span + 1;
-        const int64_t c1 = min((int64_t)nchunks - 1, cur / span);
-        for (int64_t c = c0; c <= c1; ++c) cb[c] = (uint32_t)b;
-    }
-    if (threadIdx.x == 0) cb[nchunks] = (uint32_t)nb1;
+    if (b0 < nb1) bs[b0] = e;
+    if (b1 < nb1) bs[b1] = e + v0;
+    if (threadIdx.x == 0) bs[nb1] = (uint32_t)n;
+    if (!biglist) return;
+    if (b0 < nb1 && v0 > (uint32_t)kG2BinCap) biglist[atomicAdd(bigcount, 1u)] = (uint32_t)t * nb1 + b0;
+    if (b1 < nb1 && v1 > (uint32_t)kG2BinCap) biglist[atomicAdd(bigcount, 1u)] = (uint32_t)t * nb1 + b1;
 }
 
 // Stable scatter by the L1 digit, persistent: CTA c takes work items c, c + grid, ...
@@ -550,21 +538,23 @@ __global__ void __launch_bounds__(kSThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
-// L2: per-bin sort + run-length encoding + chained bucket numbering
+// L2: per-bin sort, run-length encoding and chained bucket numbering (wide keys)
 // ---------------------------------------------------------------------------
 struct G2Args {
     const uint64_t* keys;       // L1 output [L][n]
     const uint32_t* ids;        // L1 output [L][n]
     const uint32_t* binstart;   // [L][nb1+1]
-    unsigned long long* state;  // [L][nb1] look-back words: (flag << 32) | count
-    uint32_t* scratch;          // [L][2n] permutation ping-pong of bins too large for shared memory
+    unsigned long long* state;  // (unused by the wide-key path)
+    uint32_t* scratch;          // [L][2n] permutation ping-pong of bins larger than kG2BinCap
     const L1Spec* spec;         // [L]
     int64_t n;
-    int nb1;
+    int L;
+    int nb1;                    // L1 bins per table (= numbering units per table)
     uint32_t id_base;           // ids of a table are id_base + row
-    unsigned long long* prof;   // diagnostics (LSH_G2_PROF): per-phase clock sums, nullptr = off
-    int nchunks;                // L2 chunks per table
-    const uint32_t* chunkbin;   // [L][nchunks+1] first L1 bin of every chunk
+    const uint32_t* biglist;    // t * nb1 + bin of every bin larger than kG2BinCap
+    const uint32_t* bigcount;   // [1] entries of biglist
+    uint32_t* binheads;         // [L][nb1] buckets per bin
+    uint32_t* binbase;          // [L][nb1] bucket number of each bin's first bucket
     IndexDev out;
 };
 
@@ -660,22 +650,6 @@ struct ShiftDigit {
     int sh;
     __device__ __forceinline__ uint32_t operator()(uint64_t k) const { return (uint32_t)(k >> sh) & 255u; }
 };
-// (L1 bin inside the chunk, the next `w` key bits below the L1 digit at shift `sh`)
-// A contiguous L1 digit sits directly above the window (its lowest bit is the top of
-// `below`), so (digit, window) is one bit field: shift, mask, subtract bin0.
-struct ChunkDigit {
-    L1Spec sp;
-    uint32_t bin0;
-    int w, sh;
-    uint32_t fmask, fsub;
-    __device__ __forceinline__ ChunkDigit(const L1Spec& s, uint32_t b0, int w_, int sh_)
-        : sp(s), bin0(b0), w(w_), sh(sh_), fmask((1u << (w_ + s.nbits)) - 1u), fsub(b0 << w_) {}
-    __device__ __forceinline__ uint32_t operator()(uint64_t k) const {
-        if (sp.shift >= 0) return ((uint32_t)(k >> sh) & fmask) - fsub;
-        return ((l1_digit(k, sp) - bin0) << w) | ((uint32_t)(k >> sh) & ((1u << w) - 1u));
-    }
-};
-
 template <typename PT, typename CT, typename DF = ShiftDigit, typename KE = uint64_t>
 __device__ void cta_digit_pass(const KE* K, const PT* src, PT* dst, int64_t len, DF df, CT* wcnt,
                                uint32_t* ws) {
@@ -742,79 +716,6 @@ __device__ void cta_lsd(const KE* K, PT*& cur, PT* b0, PT* b1, int64_t len, int 
     }
 }
 
-// Bucket count, chained numbering, and the outputs of one bin.  Each thread owns
-// a run of consecutive sorted positions: one block scan numbers the buckets.
-// `published`: this chunk's bucket count was already posted to the look-back state
-// (the id write-out by the other warps overlaps warp 0's look-back either way).
-template <typename PT>
-__device__ void cta_emit(const uint64_t* K, const uint32_t* ID, const PT* perm, int64_t len, int64_t lo, int t,
-                         int bin, const G2Args& a, uint32_t* ws, uint32_t* bc, bool published = false,
-                         const unsigned long long* pre = nullptr) {
-    const int64_t vp = (len + kG2Threads - 1) / kG2Threads;
-    const int64_t r0 = min(len, (int64_t)threadIdx.x * vp), r1 = min(len, r0 + vp);
-    uint32_t u = 0;
-    {
-        uint64_t prev = r0 > 0 ? K[pget(perm, r0 - 1)] : 0ull;
-        for (int64_t r = r0; r < r1; ++r) {
-            const uint64_t k = K[pget(perm, r)];
-            u += (r == 0 || k != prev) ? 1u : 0u;
-            prev = k;
-        }
-    }
-    uint32_t utot;
-    const uint32_t ex = block_excl_scan<kG2Threads>(u, ws, &utot);
-    if (threadIdx.x < 32) {
-        const uint32_t p0 = chained_prefix_warp(a.state + (int64_t)t * a.nchunks, bin, utot, published, pre);
-        if (threadIdx.x == 0) *bc = p0;
-    }
-    const int64_t n = a.n;
-    uint32_t* od = a.out.ids + (int64_t)t * n + lo;
-    for (int64_t r = threadIdx.x; r < len; r += kG2Threads) od[r] = ID[pget(perm, r)];
-    __syncthreads();
-    const uint32_t base = *bc;
-    uint64_t* uk = a.out.ukeys + (int64_t)t * n;
-    uint32_t* of = a.out.offs + (int64_t)t * (n + 1);
-    {
-        uint32_t ub = base + ex;
-        uint64_t prev = r0 > 0 ? K[pget(perm, r0 - 1)] : 0ull;
-        for (int64_t r = r0; r < r1; ++r) {
-            const uint64_t k = K[pget(perm, r)];
-            if (r == 0 || k != prev) {
-                uk[ub] = k;
-                of[ub] = (uint32_t)(lo + r);
-                ++ub;
-            }
-            prev = k;
-        }
-    }
-    if (threadIdx.x == 0 && bin == a.nchunks - 1) {
-        a.out.nb[t] = base + utot;
-        of[base + utot] = (uint32_t)n;
-    }
-}
-
-// OR / AND of per-thread key aggregates over the block (red pre-initialised to {0, ~0}).
-__device__ __forceinline__ uint64_t cta_varying_from(uint64_t o, uint64_t an, unsigned long long* red) {
-    __syncthreads();   // a previous call's reset of red is visible
-#pragma unroll
-    for (int s = 16; s > 0; s >>= 1) {
-        o |= __shfl_xor_sync(0xffffffffu, o, s);
-        an &= __shfl_xor_sync(0xffffffffu, an, s);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        atomicOr(&red[0], (unsigned long long)o);
-        atomicAnd(&red[1], (unsigned long long)an);
-    }
-    __syncthreads();
-    const uint64_t v = red[0] ^ red[1];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        red[0] = 0ull;
-        red[1] = ~0ull;
-    }
-    return v;
-}
-
 // Order a permutation range by id when its items are in L1 order: the wide-key L1
 // pass writes each tile's items of a bin as one run, bins in order and tiles in
 // order inside a bin, ids shuffled inside a run.  Along any stable sub-range the run
@@ -863,257 +764,15 @@ __device__ void cta_sort_tile_runs(const uint32_t* ID, const uint64_t* K, const 
     __syncthreads();
 }
 
-#define G2_MARK(i)                                                             \
-    do {                                                                       \
-        if (a.prof && threadIdx.x == 0) {                                      \
-            const long long now = clock64();                                   \
-            atomicAdd(a.prof + (i), (unsigned long long)(now - g2_t0));        \
-            g2_t0 = now;                                                       \
-        }                                                                      \
-    } while (0)
-
-__global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
-    long long g2_t0 = clock64();
-    extern __shared__ __align__(16) unsigned char g2_dsm[];
-    __shared__ uint32_t ws[32];
-    __shared__ uint32_t bc;
-    __shared__ int lst[2 * kG2Long];
-    __shared__ int nlst;
-    __shared__ unsigned long long red[2];
-    __shared__ uint32_t cls_cnt[3];
-    __shared__ uint32_t s_heads;
-    __shared__ uint32_t bm[kG2Cap / 32];
-    // Work unit: chunk c = the whole L1 bins whose start lies in [c*S, (c+1)*S); its
-    // items are contiguous and sorting them by the full key sorts them in place.
-    const int t = blockIdx.x, bin = blockIdx.y;   // tables interleaved: short look-back chains
+// Bins larger than kG2BinCap (skewed codes: many equal keys), on global memory: a
+// stable 3-way split around a dominant key, id order by tile runs, then stable 8-bit
+// passes over the varying key digits.  The sorted permutation ends in p0 (scratch).
+__device__ void big_bin_sort(const G2Args& a, int t, int64_t lo, int64_t len, unsigned char* g2_dsm, uint32_t* ws,
+                             unsigned long long* red, uint32_t* cls_cnt) {
     const int64_t n = a.n;
-    const uint32_t* bs = a.binstart + (int64_t)t * (a.nb1 + 1);
-    const int bin_lo = a.chunkbin[(int64_t)t * (a.nchunks + 1) + bin];
-    const int bin_hi = a.chunkbin[(int64_t)t * (a.nchunks + 1) + bin + 1];
-    const int64_t lo = bs[bin_lo];
-    const int64_t len = (int64_t)bs[bin_hi] - lo;
     const uint64_t* gk = a.keys + (int64_t)t * n + lo;
     const uint32_t* gi = a.ids + (int64_t)t * n + lo;
     const L1Spec sp = a.spec[t];
-    if (threadIdx.x == 0) {
-        red[0] = 0ull;
-        red[1] = ~0ull;
-        nlst = 0;
-    }
-
-    if (len <= kG2Cap) {
-        uint64_t* sk = reinterpret_cast<uint64_t*>(g2_dsm);                   // [cap]
-        uint32_t* si = reinterpret_cast<uint32_t*>(g2_dsm + kG2Cap * 8);      // [cap]
-        uint16_t* pa = reinterpret_cast<uint16_t*>(g2_dsm + kG2Cap * 12);     // [cap]
-        uint16_t* pb = pa + kG2Cap;                                           // [cap]
-        uint32_t* cnt = reinterpret_cast<uint32_t*>(pb + kG2Cap);             // [2048] two u16 counters per word
-        // the bits below the L1 digit (the table's varying-bit mask chooses the window;
-        // a chunk whose keys are constant there still sorts correctly, through the
-        // long-segment path)
-        const int hb = (sp.nbits == 0 || len == 0) ? 0 : 64 - __clzll((long long)sp.below);
-        const int G = bin_hi - bin_lo;
-        const int gb = G > 1 ? 32 - __clz(G - 1) : 0;    // bits of the bin index inside the chunk
-        // (1) counting scatter on D <= 12 bits: (bin in chunk, top Dw varying bits below
-        //     the digit); not stable, fixed in (2).  Counted while the chunk is loaded.
-        const int Dw = min(12 - gb, hb);
-        const int D = gb + Dw;
-        const int sh = hb - Dw;
-        const ChunkDigit cd(sp, (uint32_t)bin_lo, Dw, sh);
-        const int nw = (1 << D) > 2 ? (1 << D) >> 1 : 1;
-        for (int i = threadIdx.x; i < nw; i += kG2Threads) cnt[i] = 0u;
-        if (threadIdx.x == 0) s_heads = 0u;
-        __syncthreads();
-        {
-            constexpr int PT = kG2Cap / kG2Threads / 2;   // 4 items per thread per half
-#pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-                if (h2 * PT * kG2Threads >= len) break;
-                uint64_t kr[PT];
-                uint32_t ir[PT];
-#pragma unroll
-                for (int j = 0; j < PT; ++j) {
-                    const int i = threadIdx.x + (h2 * PT + j) * kG2Threads;
-                    if (i < len) {
-                        kr[j] = __ldg(gk + i);
-                        ir[j] = __ldg(gi + i);
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < PT; ++j) {
-                    const int i = threadIdx.x + (h2 * PT + j) * kG2Threads;
-                    if (i < len) {
-                        sk[i] = kr[j];
-                        si[i] = ir[j];
-                        const uint32_t dg = cd(kr[j]);
-                        atomicAdd(&cnt[dg >> 1], 1u << ((dg & 1u) << 4));
-                    }
-                }
-            }
-        }
-        __syncthreads();
-        uint16_t* cur = nullptr;
-        bool published = false;
-        unsigned long long lbpre = 0;
-        if (len > 1) {   // (the L1 pass leaves ids unordered inside a bin: always sort)
-            G2_MARK(0);   // load + digit counts
-            {
-                const int WPT = (nw + kG2Threads - 1) / kG2Threads;
-                uint32_t sm = 0;
-                for (int j = 0; j < WPT; ++j) {
-                    const int w = threadIdx.x * WPT + j;
-                    if (w < nw) {
-                        const uint32_t c = cnt[w];
-                        sm += (c & 0xffffu) + (c >> 16);
-                    }
-                }
-                uint32_t ex = block_excl_scan<kG2Threads>(sm, ws, nullptr);
-                for (int j = 0; j < WPT; ++j) {
-                    const int w = threadIdx.x * WPT + j;
-                    if (w < nw) {
-                        const uint32_t c = cnt[w], c0 = c & 0xffffu;
-                        cnt[w] = ex | ((ex + c0) << 16);
-                        ex += c0 + (c >> 16);
-                    }
-                }
-            }
-            __syncthreads();
-            for (int i = threadIdx.x; i < len; i += kG2Threads) {
-                const uint32_t dg = cd(sk[i]);
-                const uint32_t hs = (dg & 1u) << 4;
-                const uint32_t old = atomicAdd(&cnt[dg >> 1], 1u << hs);
-                pa[(old >> hs) & 0xffffu] = (uint16_t)i;
-            }
-            __syncthreads();
-            G2_MARK(1);   // counting scatter
-            // (2) order inside segments of equal key >> sh by (key, position): O(s) ranks for
-            //     short segments; long ones by a position bitmap, then stable passes on the
-            //     bits below sh if they vary there
-            const uint16_t* src = pa;
-            uint16_t* dst = pb;
-            // after the scatter, counter word w holds the END positions of digits 2w, 2w+1;
-            // a segment of equal key >> sh is exactly one digit bucket
-            auto digit_end = [&](uint32_t dg) { return (cnt[dg >> 1] >> ((dg & 1u) << 4)) & 0xffffu; };
-            uint32_t heads = 0;
-            for (int r = threadIdx.x; r < len; r += kG2Threads) {
-                const uint32_t me = src[r];
-                const uint64_t kv = sk[me];
-                const uint32_t dg = cd(kv);
-                const int e = (int)digit_end(dg);
-                const int h = dg ? (int)digit_end(dg - 1) : 0;
-                if (e - h == 1) {
-                    dst[r] = (uint16_t)me;
-                    ++heads;
-                    continue;
-                }
-                if (e - h > kG2Seg) {   // long segment: position bitmap below
-                    if (r == h) {
-                        const int slot = atomicAdd(&nlst, 1);
-                        if (slot < kG2Long) {
-                            lst[2 * slot] = h;
-                            lst[2 * slot + 1] = e;
-                        }
-                    }
-                    continue;
-                }
-                const uint32_t idm = si[me];
-                int rank = 0;
-                bool dup = false;   // an equal key with a smaller id: not the bucket's head
-                for (int j = h; j < e; ++j) {
-                    const uint32_t sj = src[j];
-                    const uint64_t kj = sk[sj];
-                    const bool eqs = kj == kv && si[sj] < idm;
-                    rank += (kj < kv || eqs) ? 1 : 0;
-                    dup |= eqs;
-                }
-                dst[h + rank] = (uint16_t)me;
-                heads += dup ? 0u : 1u;
-            }
-            heads = __reduce_add_sync(0xffffffffu, heads);
-            if ((threadIdx.x & 31) == 0) atomicAdd(&s_heads, heads);
-            __syncthreads();
-            // no long segment: every bucket head is known, so post this chunk's bucket
-            // count now; later chunks' look-backs need not wait for this chunk's emit
-            published = nlst == 0;
-            if (published && threadIdx.x < 32) {
-                if (threadIdx.x == 0)
-                    st_release(a.state + (int64_t)t * a.nchunks + bin, ((bin == 0 ? 2ull : 1ull) << 32) | s_heads);
-                // first look-back round issued now; consumed after the emit's scan
-                lbpre = lookback_preload(a.state + (int64_t)t * a.nchunks, bin);
-            }
-            G2_MARK(2);   // segment ranks
-            const int nl = min(nlst, kG2Long);
-            uint16_t* wc = reinterpret_cast<uint16_t*>(cnt);   // [kG2Warps][256] for the stable passes
-            for (int q = 0; q < nl; ++q) {
-                const int h = lst[2 * q], e = lst[2 * q + 1];
-                // (key, id) order for a long segment: (1) position bitmap -> L1 order, whose
-                // (bin, tile) runs ascend; (2) rank by id inside each run (O(run length));
-                // (3) stable passes over the key bits below sh if they vary here
-                for (int w = threadIdx.x; w < kG2Cap / 32; w += kG2Threads) bm[w] = 0u;
-                __syncthreads();
-                uint64_t so = 0, sa = ~0ull;
-                for (int r = h + threadIdx.x; r < e; r += kG2Threads) {
-                    const uint32_t pp = src[r];
-                    atomicOr(&bm[pp >> 5], 1u << (pp & 31u));
-                    so |= sk[pp];
-                    sa &= sk[pp];
-                }
-                __syncthreads();
-                {
-                    const uint32_t c = threadIdx.x < kG2Cap / 32 ? (uint32_t)__popc(bm[threadIdx.x]) : 0u;
-                    uint32_t ex = block_excl_scan<kG2Threads>(c, ws, nullptr);
-                    if (threadIdx.x < kG2Cap / 32) {
-                        uint32_t bits = bm[threadIdx.x];
-                        uint32_t o2 = h + ex;
-                        while (bits) {
-                            const int b = __ffs(bits) - 1;
-                            pa[o2++] = (uint16_t)(threadIdx.x * 32 + b);   // pa = spare (src consumed)
-                            bits &= bits - 1u;
-                        }
-                    }
-                }
-                __syncthreads();
-                auto run_of = [&](int r) {
-                    const uint32_t pp = pa[r];
-                    return ((uint64_t)l1_digit(sk[pp], sp) << 32) | ((si[pp] - a.id_base) >> 13);
-                };
-                for (int r = h + threadIdx.x; r < e; r += kG2Threads) {
-                    const uint64_t run = run_of(r);
-                    int rh = h, rb = r;          // first index of the run (runs ascend)
-                    while (rh < rb) {
-                        const int mid = (rh + rb) >> 1;
-                        if (run_of(mid) < run) rh = mid + 1;
-                        else rb = mid;
-                    }
-                    int re = r + 1, eb = e;       // one past its last index
-                    while (re < eb) {
-                        const int mid = (re + eb) >> 1;
-                        if (run_of(mid) == run) re = mid + 1;
-                        else eb = mid;
-                    }
-                    const uint32_t me = pa[r], idm = si[me];
-                    int rank = 0;
-                    for (int j = rh; j < re; ++j) rank += si[pa[j]] < idm ? 1 : 0;
-                    dst[rh + rank] = (uint16_t)me;
-                }
-                __syncthreads();
-                const uint64_t vk = cta_varying_from(so, sa, red) & ((sh > 0) ? ((1ull << sh) - 1ull) : 0ull);
-                if (!vk) continue;   // all keys equal: id order is final
-                uint16_t* c2 = dst + h;
-                cta_lsd<uint16_t, uint16_t, uint64_t>(sk, c2, dst + h, pa + h, e - h, sh, vk, wc, ws);
-                if (c2 != dst + h) {
-                    for (int r = threadIdx.x; r < e - h; r += kG2Threads) dst[h + r] = c2[r];
-                    __syncthreads();
-                }
-            }
-            cur = dst;
-        }
-        G2_MARK(3);   // long segments
-        cta_emit<uint16_t>(sk, si, cur, len, lo, t, bin, a, ws, &bc, published, published ? &lbpre : nullptr);
-        G2_MARK(4);   // emit (incl. look-back)
-        return;
-    }
-
-    // ---- bin larger than shared memory: the same algorithm on global memory ----
     uint32_t* wc = reinterpret_cast<uint32_t*>(g2_dsm);  // [kG2Warps][256] u32
     uint32_t* p0 = a.scratch + (int64_t)t * 2 * n + lo;
     uint32_t* p1 = p0 + n;
@@ -1205,7 +864,368 @@ __global__ void __launch_bounds__(kG2Threads, 3) g2_sort(G2Args a) {
             cta_lsd<uint32_t, uint32_t>(gk, cur, p0, p1, len, sh1, varying, wc, ws);
         }
     }
-    cta_emit<uint32_t>(gk, gi, cur, len, lo, t, bin, a, ws, &bc);
+    if (cur != p0) {
+        for (int64_t r = threadIdx.x; r < len; r += kG2Threads) p0[r] = cur[r];
+        __threadfence_block();
+        __syncthreads();
+    }
+}
+
+// Big bins: sort (permutation in p0), write the bin's ids in final order and its
+// bucket count; g2e emits its ukeys / offs through the permutation.  Persistent over
+// the big-bin list.
+__global__ void __launch_bounds__(kG2Threads) g2_big(G2Args a) {
+    extern __shared__ __align__(16) unsigned char g2_dsm[];
+    __shared__ uint32_t ws[32];
+    __shared__ unsigned long long red[2];
+    __shared__ uint32_t cls_cnt[3];
+    const uint32_t cnt = *a.bigcount;
+    for (uint32_t i = blockIdx.x; i < cnt; i += gridDim.x) {
+        const uint32_t e = a.biglist[i];
+        const int t = (int)(e / (uint32_t)a.nb1), bin = (int)(e % (uint32_t)a.nb1);
+        const uint32_t* bs = a.binstart + (int64_t)t * (a.nb1 + 1);
+        const int64_t lo = bs[bin], len = (int64_t)bs[bin + 1] - lo;
+        if (threadIdx.x == 0) {
+            red[0] = 0ull;
+            red[1] = ~0ull;
+        }
+        __syncthreads();
+        big_bin_sort(a, t, lo, len, g2_dsm, ws, red, cls_cnt);
+        const uint64_t* gk = a.keys + (int64_t)t * a.n + lo;
+        const uint32_t* gi = a.ids + (int64_t)t * a.n + lo;
+        const uint32_t* p0 = a.scratch + (int64_t)t * 2 * a.n + lo;
+        uint32_t* od = a.out.ids + (int64_t)t * a.n + lo;
+        uint32_t heads = 0;
+        for (int64_t r = threadIdx.x; r < len; r += kG2Threads) {
+            const uint32_t pr = p0[r];
+            od[r] = gi[pr];
+            heads += (r == 0 || gk[p0[r - 1]] != gk[pr]) ? 1u : 0u;
+        }
+        uint32_t tot;
+        block_excl_scan<kG2Threads>(heads, ws, &tot);
+        if (threadIdx.x == 0) a.binheads[(int64_t)t * a.nb1 + bin] = tot;
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// g2a: one CTA (4 warps) per L1 bin of <= kG2aCap items (larger: g2_big), no
+// cross-bin dependency, many CTAs resident per SM.  In shared memory:
+//   (1) counting scatter on the D <= 12 key bits right below the L1 digit (the keys
+//       of a bin agree on every bit above), ranks from the counting atomics;
+//   (2) a digit holding one item (for fingerprints ~3/4 of them) places it at its
+//       final position at once; the items of a shared digit are ranked among its
+//       members by (key, id), and segments longer than kG2aLong (duplicate-heavy
+//       codes) are bitonic-sorted; a bucket head is an item with no equal key of
+//       smaller id;
+//   (3) ids and the sorted keys stream out coalesced (keys in place, over the bin's
+//       L1 output), plus the bin's bucket count.
+// g2s scans the counts per table, g2e numbers the buckets from the sorted keys.
+// ---------------------------------------------------------------------------
+constexpr int kG2aT = 128;
+constexpr int kG2aW = kG2aT / 32;
+constexpr int kG2aIPT = 10;
+constexpr int kG2aCap = kG2aT * kG2aIPT;      // 1280 items
+constexpr int kG2aD = 12;                      // digit bits (4096 counters)
+constexpr int kG2aCW = 1 << (kG2aD - 1);       // counter words (two u16 counters each)
+constexpr int kG2aLong = 64;                   // longest segment ranked item by item
+constexpr int kG2aLongMax = kG2aCap / kG2aLong;
+static_assert(kG2aCap == kG2BinCap, "big-bin threshold");
+
+struct __align__(16) G2aSmem {
+    uint64_t sk[kG2aCap];
+    uint32_t si[kG2aCap];
+    uint32_t cnt[kG2aCW];   // digit counters -> digit starts -> long-segment scratch
+    uint32_t ws[kG2aW];
+    uint32_t lseg[kG2aLongMax];
+    uint32_t nlong, heads;
+};
+
+// Bitonic sort of the items at [s0, s0 + len) of S by (key, id): fin[p] = final
+// position of the item at p, bit 15 = bucket head.
+__device__ void g2a_long_segment(G2aSmem& S, uint32_t s0, uint32_t len, uint16_t* perm, uint16_t* fin) {
+    int P = 1;
+    while (P < (int)len) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += kG2aT) perm[i] = (uint16_t)(i < (int)len ? s0 + i : 0xffffu);
+    __syncthreads();
+    auto less = [&](uint16_t x, uint16_t y) {   // pads (0xffff) sort last
+        if (x == 0xffffu) return false;
+        if (y == 0xffffu) return true;
+        const uint64_t kx = S.sk[x], ky = S.sk[y];
+        return kx < ky || (kx == ky && S.si[x] < S.si[y]);
+    };
+    for (int size = 2; size <= P; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < (P >> 1); i += kG2aT) {
+                const int lo = 2 * stride * (i / stride) + (i % stride), hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const uint16_t x = perm[lo], y = perm[hi];
+                if (less(y, x) == up) {
+                    perm[lo] = y;
+                    perm[hi] = x;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int j = threadIdx.x; j < (int)len; j += kG2aT) {
+        const uint16_t pj = perm[j];
+        const bool head = j == 0 || S.sk[perm[j - 1]] != S.sk[pj];
+        fin[pj] = (uint16_t)((s0 + j) | (head ? 0x8000u : 0u));
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kG2aT) g2a(G2Args a) {
+    extern __shared__ __align__(16) unsigned char g2a_dsm[];
+    G2aSmem& S = *reinterpret_cast<G2aSmem*>(g2a_dsm);
+    const int u = threadIdx.x, lane = u & 31, wu = u >> 5;
+    const int nb1 = a.nb1;
+    const int64_t n = a.n;
+    const int t = (int)(blockIdx.x / nb1), bin = (int)(blockIdx.x % nb1);   // table-major
+    const uint32_t* bs = a.binstart + (int64_t)t * (nb1 + 1);
+    const int64_t lo = bs[bin];
+    const int len = (int)((int64_t)bs[bin + 1] - lo);
+    if (len > kG2aCap) return;   // g2_big's
+    uint64_t* gk = const_cast<uint64_t*>(a.keys) + (int64_t)t * n + lo;
+    const uint32_t* gi = a.ids + (int64_t)t * n + lo;
+    uint64_t kr[kG2aIPT];
+    uint32_t ir[kG2aIPT], dr[kG2aIPT];
+#pragma unroll
+    for (int j = 0; j < kG2aIPT; ++j) {
+        const int i = u + j * kG2aT;
+        if (i < len) {
+            kr[j] = __ldcs(gk + i);
+            ir[j] = __ldcs(gi + i);
+        }
+    }
+    {
+        uint4* c4 = reinterpret_cast<uint4*>(S.cnt);
+        for (int w = u; w < kG2aCW / 4; w += kG2aT) c4[w] = make_uint4(0u, 0u, 0u, 0u);
+        if (u == 0) {
+            S.nlong = 0u;
+            S.heads = 0u;
+        }
+    }
+    const L1Spec sp = a.spec[t];
+    // keys of the bin agree on every bit at or above the lowest L1 digit bit (hb)
+    const int hb = sp.below == 0 ? 0 : 64 - __clzll((long long)sp.below);
+    const int D = min(kG2aD, hb), sh = hb - D;
+    const uint32_t dmask = (1u << D) - 1u;
+    __syncthreads();
+    // (1) digit counts; the atomic's old value is the item's rank inside its digit
+#pragma unroll
+    for (int j = 0; j < kG2aIPT; ++j) {
+        const int i = u + j * kG2aT;
+        if (i < len) {
+            const uint32_t d = (uint32_t)(kr[j] >> sh) & dmask;
+            const uint32_t hs = (d & 1u) << 4;
+            const uint32_t old = atomicAdd(&S.cnt[d >> 1], 1u << hs);
+            dr[j] = (d << 16) | ((old >> hs) & 0xffffu);
+        }
+    }
+    __syncthreads();
+    {
+        // exclusive scan of the 4096 counters: thread u owns words [16u, 16u + 16)
+        constexpr int WPT = kG2aCW / kG2aT;
+        uint32_t wv[WPT], sum = 0;
+        const uint4* c4 = reinterpret_cast<const uint4*>(S.cnt + WPT * u);
+#pragma unroll
+        for (int q4 = 0; q4 < WPT / 4; ++q4) {
+            const uint4 v = c4[q4];
+            wv[4 * q4] = v.x;
+            wv[4 * q4 + 1] = v.y;
+            wv[4 * q4 + 2] = v.z;
+            wv[4 * q4 + 3] = v.w;
+        }
+#pragma unroll
+        for (int qq = 0; qq < WPT; ++qq) sum += (wv[qq] & 0xffffu) + (wv[qq] >> 16);
+        uint32_t x = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) S.ws[wu] = x;
+        __syncthreads();
+        uint32_t ex = x - sum;
+#pragma unroll
+        for (int w = 0; w < kG2aW; ++w) ex += w < wu ? S.ws[w] : 0u;
+        uint4* o4 = reinterpret_cast<uint4*>(S.cnt + WPT * u);
+#pragma unroll
+        for (int q4 = 0; q4 < WPT / 4; ++q4) {
+            uint32_t o[4];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                const uint32_t w = wv[4 * q4 + jj], c0 = w & 0xffffu;
+                o[jj] = ex | ((ex + c0) << 16);
+                ex += c0 + (w >> 16);
+            }
+            o4[q4] = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+    }
+    __syncthreads();
+    // (2) place: an item alone in its digit is final; the others go to their digit's
+    // region (arbitrary order) and are ranked below.  dr: kDone, or (s0 << 16) | len
+    // for a short segment, or kLong | position for a long one
+    constexpr uint32_t kDone = 0xffffffffu, kLong = 0x80000000u;
+    uint32_t heads = 0;
+#pragma unroll
+    for (int j = 0; j < kG2aIPT; ++j) {
+        const int i = u + j * kG2aT;
+        if (i < len) {
+            const uint32_t d = dr[j] >> 16, r = dr[j] & 0xffffu;
+            const uint32_t w0 = S.cnt[d >> 1];
+            const uint32_t s0 = (w0 >> ((d & 1u) << 4)) & 0xffffu;
+            const uint32_t s1 = d == dmask ? (uint32_t)len
+                                           : ((d & 1u) ? (S.cnt[(d + 1) >> 1] & 0xffffu) : (w0 >> 16));
+            const uint32_t p = s0 + r;
+            S.sk[p] = kr[j];
+            S.si[p] = ir[j];
+            if (s1 - s0 == 1) {
+                dr[j] = kDone;
+                ++heads;
+            } else if (s1 - s0 <= (uint32_t)kG2aLong) {
+                dr[j] = (s0 << 16) | (s1 - s0);
+            } else {
+                dr[j] = kLong | p;
+                if (r == 0) S.lseg[atomicAdd(&S.nlong, 1u)] = (s0 << 16) | (s1 - s0);
+            }
+        }
+    }
+    __syncthreads();
+    // rank inside shared digits by (key, id); f = final position
+#pragma unroll
+    for (int j = 0; j < kG2aIPT; ++j) {
+        const int i = u + j * kG2aT;
+        if (i < len && dr[j] != kDone && !(dr[j] & kLong)) {
+            const uint32_t s0 = dr[j] >> 16, sl = dr[j] & 0xffffu;
+            const uint64_t k = kr[j];
+            const uint32_t id = ir[j];
+            uint32_t f = s0, dup = 0;
+            for (uint32_t qq = s0; qq < s0 + sl; ++qq) {
+                const uint64_t kq = S.sk[qq];
+                const uint32_t iq = S.si[qq];
+                const bool eq_lt = kq == k && iq < id;
+                f += (kq < k || eq_lt) ? 1u : 0u;
+                dup |= eq_lt ? 1u : 0u;
+            }
+            dr[j] = f;   // < kCap: neither kDone nor kLong
+            heads += dup ^ 1u;
+        }
+    }
+    const uint32_t nl = S.nlong;   // complete: appended before the last barrier
+    if (nl) {
+        // duplicate-heavy segments: bitonic sort by (key, id) in the (free) counter area
+        uint16_t* perm = reinterpret_cast<uint16_t*>(S.cnt);
+        uint16_t* fin = perm + 2 * kG2aCap;
+        for (uint32_t g = 0; g < nl; ++g) g2a_long_segment(S, S.lseg[g] >> 16, S.lseg[g] & 0xffffu, perm, fin);
+#pragma unroll
+        for (int j = 0; j < kG2aIPT; ++j) {
+            const int i = u + j * kG2aT;
+            if (i < len && dr[j] != kDone && (dr[j] & kLong)) {
+                const uint32_t fv = fin[dr[j] & 0xffffu];
+                dr[j] = fv & 0x7fffu;
+                heads += fv >> 15;
+            }
+        }
+    }
+    heads = __reduce_add_sync(0xffffffffu, heads);
+    if (lane == 0) atomicAdd(&S.heads, heads);
+    __syncthreads();   // every read of the digit regions is done
+#pragma unroll
+    for (int j = 0; j < kG2aIPT; ++j) {
+        const int i = u + j * kG2aT;
+        if (i < len && dr[j] != kDone) {
+            S.sk[dr[j]] = kr[j];
+            S.si[dr[j]] = ir[j];
+        }
+    }
+    __syncthreads();
+    // (3) ids and sorted keys out (coalesced; keys in place over the bin's L1 output)
+    uint32_t* od = a.out.ids + (int64_t)t * n + lo;
+    for (int p = u; p < len; p += kG2aT) {
+        od[p] = S.si[p];
+        __stcs(gk + p, S.sk[p]);
+    }
+    if (u == 0) a.binheads[(int64_t)t * nb1 + bin] = S.heads;
+}
+
+// g2s: per table, bucket base of every bin = exclusive scan of the bins' bucket
+// counts; nb[t] and the closing offs[nb] = n.
+__global__ void __launch_bounds__(1024) g2s(G2Args a) {
+    __shared__ uint32_t ws[32];
+    const int t = blockIdx.x, nb1 = a.nb1;
+    const uint32_t* hc = a.binheads + (int64_t)t * nb1;
+    uint32_t* bb = a.binbase + (int64_t)t * nb1;
+    constexpr int PT = 2;   // nb1 <= 2048
+    uint32_t v[PT], s = 0;
+#pragma unroll
+    for (int j = 0; j < PT; ++j) {
+        const int b = threadIdx.x * PT + j;
+        v[j] = b < nb1 ? hc[b] : 0u;
+        s += v[j];
+    }
+    uint32_t tot;
+    uint32_t ex = block_excl_scan<1024>(s, ws, &tot);
+#pragma unroll
+    for (int j = 0; j < PT; ++j) {
+        const int b = threadIdx.x * PT + j;
+        if (b < nb1) bb[b] = ex;
+        ex += v[j];
+    }
+    if (threadIdx.x == 0) {
+        a.out.nb[t] = tot;
+        a.out.offs[(int64_t)t * (a.n + 1) + tot] = (uint32_t)a.n;
+    }
+}
+
+// g2e: bucket numbering of one bin from its sorted keys: a head is a key that differs
+// from its predecessor (the first key of a bin always does: bins differ in the L1
+// digit); ukeys[base + #heads before] = key, offs[...] = its position.  Big bins read
+// their keys through g2_big's permutation.
+constexpr int kG2eT = 256;
+__global__ void __launch_bounds__(kG2eT) g2e(G2Args a) {
+    __shared__ uint32_t wc[kG2eT / 32];
+    const int u = threadIdx.x, lane = u & 31, wu = u >> 5;
+    const int nb1 = a.nb1;
+    const int64_t n = a.n;
+    const int t = (int)(blockIdx.x / nb1), bin = (int)(blockIdx.x % nb1);
+    const uint32_t* bs = a.binstart + (int64_t)t * (nb1 + 1);
+    const int64_t lo = bs[bin];
+    const int len = (int)((int64_t)bs[bin + 1] - lo);
+    if (len == 0) return;
+    const uint64_t* gk = a.keys + (int64_t)t * n + lo;
+    const uint32_t* perm = len > kG2aCap ? a.scratch + (int64_t)t * 2 * n + lo : nullptr;
+    auto key = [&](int p) { return perm ? gk[perm[p]] : __ldcs(gk + p); };
+    uint32_t b = a.binbase[(int64_t)t * nb1 + bin];
+    uint64_t* uk = a.out.ukeys + (int64_t)t * n;
+    uint32_t* of = a.out.offs + (int64_t)t * (n + 1);
+    for (int p0 = 0; p0 < len; p0 += kG2eT) {
+        const int p = p0 + u;
+        const bool v = p < len;
+        const uint64_t k = v ? key(p) : 0ull;
+        uint64_t kp = __shfl_up_sync(0xffffffffu, k, 1);
+        if (lane == 0 && p > 0 && v) kp = key(p - 1);
+        const bool h = v && (p == 0 || k != kp);
+        const uint32_t m = __ballot_sync(0xffffffffu, h);
+        if (lane == 0) wc[wu] = __popc(m);
+        __syncthreads();
+        uint32_t before = 0, all = 0;
+#pragma unroll
+        for (int w = 0; w < kG2eT / 32; ++w) {
+            const uint32_t c = wc[w];
+            before += w < wu ? c : 0u;
+            all += c;
+        }
+        if (h) {
+            const uint32_t bb = b + before + __popc(m & lanemask_lt());
+            uk[bb] = k;
+            of[bb] = (uint32_t)(lo + p);
+        }
+        b += all;
+        __syncthreads();
+    }
 }
 
 // Run-length encoding of fully sorted keys (LSD path): chunk c = items
@@ -1254,26 +1274,22 @@ __global__ void __launch_bounds__(kG2Threads) g3_rle(const uint64_t* __restrict_
     }
 }
 
-// keys 8 + ids 4 + two u16 permutations per item, then the digit counters: 2048
-// words (12-bit window, two 16-bit counters per word), which also hold the per-warp
-// counts of the stable passes; the big path reuses the area for its own scratch
-static size_t g2_smem() {
-    const size_t cnt = std::max<size_t>(2048 * 4, (size_t)kG2Warps * 256 * 2);
-    return std::max<size_t>((size_t)kG2Cap * 16 + cnt, 16384 + 1024 + 16384);
-}
+// big-bin path: per-warp 8-bit digit counts (16 KB), a run bitmap (1 KB) and its
+// 8192 positions (16 KB)
+static size_t g2_big_smem() { return 16384 + 1024 + 16384; }
 
 size_t group_hist_words(int64_t n, int W) {
     return ((size_t)1 << group_l1_bits(n, W)) * group_tiles(n);
 }
 int group_bins(int64_t n, int W) { return 1 << group_l1_bits(n, W); }
-int group_chunks(int64_t n) { return (int)((n + kG2Span - 1) / kG2Span); }
+int group_rle_chunks(int64_t n) { return (int)((n + kG2Cap - 1) / kG2Cap); }
 size_t group_spec_bytes() { return sizeof(L1Spec); }
 
 // One L1 counting pass (histogram, tile scan, bin starts, stable scatter) of every
 // table by the digit of spec[0..L).
 static cudaError_t l1_pass(const uint64_t* kin, const uint32_t* iin, uint64_t* kout, uint32_t* iout, int64_t n, int L,
-                           const L1Spec* spec, int nb1, uint32_t id_base, GroupScratch& sc, int span, int nchunks,
-                           uint32_t* chunkbin, int num_sms, cudaStream_t s, bool hist_done = false,
+                           const L1Spec* spec, int nb1, uint32_t id_base, GroupScratch& sc, uint32_t* biglist,
+                           uint32_t* bigcount, int num_sms, cudaStream_t s, bool hist_done = false,
                            bool stable = true) {
     const int T = (int)group_tiles(n);
     const dim3 g1(T, L);
@@ -1287,7 +1303,7 @@ static cudaError_t l1_pass(const uint64_t* kin, const uint32_t* iin, uint64_t* k
     const int64_t warps = (int64_t)L * ((nb1 + 31) / 32);
     g1_scan<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(sc.hist, T, L, nb1, sc.tot);
     count_launch();
-    g1_binstart<<<L, 1024, 0, s>>>(sc.tot, nb1, n, sc.binstart, span, nchunks, chunkbin);
+    g1_binstart<<<L, 1024, 0, s>>>(sc.tot, nb1, n, sc.binstart, biglist, bigcount);
     count_launch();
     timing_end("group_scan", s);
     timing_begin("group_scatter", s);
@@ -1357,10 +1373,10 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
     timing_end("group_hist", s);
     if (lsd) {
         // narrow keys: full stable LSD sort on the varying bits (two passes), then RLE
-        e = l1_pass(keys, nullptr, sc.keys_a, sc.ids_a, n, L, spec, nb1, id_base, sc, 0, 0, nullptr, sc.num_sms, s);
+        e = l1_pass(keys, nullptr, sc.keys_a, sc.ids_a, n, L, spec, nb1, id_base, sc, nullptr, nullptr, sc.num_sms, s);
         if (e != cudaSuccess) return e;
         uint64_t* kb = reinterpret_cast<uint64_t*>(sc.perm);
-        e = l1_pass(sc.keys_a, sc.ids_a, kb, out.ids, n, L, spec + L, nb1, id_base, sc, 0, 0, nullptr, sc.num_sms, s);
+        e = l1_pass(sc.keys_a, sc.ids_a, kb, out.ids, n, L, spec + L, nb1, id_base, sc, nullptr, nullptr, sc.num_sms, s);
         if (e != cudaSuccess) return e;
         const int nch = (int)((n + kG2Cap - 1) / kG2Cap);
         timing_begin("group_sort", s);
@@ -1371,13 +1387,12 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
         timing_end("group_sort", s);
         return cudaGetLastError();
     }
-    const int nch = group_chunks(n);
-    e = l1_pass(keys, nullptr, sc.keys_a, sc.ids_a, n, L, spec, nb1, id_base, sc, kG2Span, nch, sc.chunkbin, sc.num_sms, s,
+    e = cudaMemsetAsync(sc.bigcount, 0, sizeof(uint32_t), s);
+    if (e != cudaSuccess) return e;
+    e = l1_pass(keys, nullptr, sc.keys_a, sc.ids_a, n, L, spec, nb1, id_base, sc, sc.biglist, sc.bigcount, sc.num_sms, s,
                 true, /*stable=*/false);
     if (e != cudaSuccess) return e;
     timing_begin("group_sort", s);
-    e = cudaMemsetAsync(sc.state, 0, sizeof(unsigned long long) * (size_t)L * nch, s);
-    if (e != cudaSuccess) return e;
     G2Args a;
     a.keys = sc.keys_a;
     a.ids = sc.ids_a;
@@ -1386,33 +1401,28 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
     a.scratch = sc.perm;
     a.spec = spec;
     a.n = n;
+    a.L = L;
     a.nb1 = nb1;
     a.id_base = id_base;
-    a.prof = nullptr;
-    static unsigned long long* g2prof = nullptr;
-    if (getenv("LSH_G2_PROF")) {
-        if (!g2prof) cudaMalloc(&g2prof, 8 * sizeof(unsigned long long));
-        cudaMemsetAsync(g2prof, 0, 8 * sizeof(unsigned long long), s);
-        a.prof = g2prof;
-    }
-    a.nchunks = nch;
-    a.chunkbin = sc.chunkbin;
+    a.biglist = sc.biglist;
+    a.bigcount = sc.bigcount;
     a.out = out;
-    const size_t sm2 = g2_smem();
-    e = cudaFuncSetAttribute(g2_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+    a.binheads = reinterpret_cast<uint32_t*>(sc.state);
+    a.binbase = a.binheads + (size_t)L * nb1;
+    const size_t smb = g2_big_smem();
+    e = cudaFuncSetAttribute(g2_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb);
     if (e != cudaSuccess) return e;
-    g2_sort<<<dim3(L, nch), kG2Threads, sm2, s>>>(a);
+    e = cudaFuncSetAttribute(g2a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(G2aSmem));
+    if (e != cudaSuccess) return e;
+    const unsigned bins = (unsigned)((int64_t)L * nb1);
+    g2_big<<<sc.num_sms, kG2Threads, smb, s>>>(a);   // bins larger than kG2aCap (usually none)
     count_launch();
-    if (a.prof) {
-        unsigned long long h[8];
-        cudaMemcpyAsync(h, a.prof, sizeof h, cudaMemcpyDeviceToHost, s);
-        cudaStreamSynchronize(s);
-        const double tot = (double)(h[0] + h[1] + h[2] + h[3] + h[4]) + 1e-9;
-        fprintf(stderr, "[g2 prof] chunks=%lld cycles/chunk: load %.0f  scatter %.0f  ranks %.0f  long %.0f  emit %.0f  (%.0f%% %.0f%% %.0f%% %.0f%% %.0f%%)\n",
-                (long long)L * nch, h[0] / (double)(L * nch), h[1] / (double)(L * nch), h[2] / (double)(L * nch),
-                h[3] / (double)(L * nch), h[4] / (double)(L * nch), 100 * h[0] / tot, 100 * h[1] / tot,
-                100 * h[2] / tot, 100 * h[3] / tot, 100 * h[4] / tot);
-    }
+    g2a<<<bins, kG2aT, sizeof(G2aSmem), s>>>(a);      // sort every bin, ids + sorted keys out
+    count_launch();
+    g2s<<<L, 1024, 0, s>>>(a);                        // bucket numbers of each bin's first bucket
+    count_launch();
+    g2e<<<bins, kG2eT, 0, s>>>(a);                    // ukeys / offs
+    count_launch();
     timing_end("group_sort", s);
     return cudaGetLastError();
 }
@@ -1542,6 +1552,7 @@ __global__ void __launch_bounds__(1024) global_offsets_kernel(const uint32_t* __
         __syncthreads();
     }
 }
+
 
 cudaError_t launch_global_offsets(const uint32_t* all, int G, int rank, int L, int B, int64_t* off, cudaStream_t s) {
     global_offsets_kernel<<<L, 1024, 0, s>>>(all, G, rank, L, B, off);

@@ -1,15 +1,11 @@
 // internal.hpp — structures shared by the host core (api.cu) and the kernel
-// launchers (sketch.cu, group.cu, dense.cu).  Not part of the C ABI.
+// launchers (sketch*.cu, group.cu, dense_tc.cu, knn.cu).  Not part of the C ABI.
 #pragma once
 
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace lshb {
-
-// Fingerprint constants of reading B10 (FNV-1a-64 + SplitMix64 finaliser).
-#define LSHB_FNV_OFFSET 0xcbf29ce484222325ull
-#define LSHB_FNV_PRIME 0x100000001b3ull
 
 // ---------------------------------------------------------------------------
 // Sparse one-nonzero-per-column projection (CS and HCS), DESIGN.md §K1.
@@ -18,6 +14,10 @@ namespace lshb {
 // bin, the run of contributing coordinates: coordinates are staged in bin-sorted
 // order (ascending coordinate inside a bin) with their sign already applied.
 // ---------------------------------------------------------------------------
+// Words per staged float4 column of the K1 tile (4 coordinates x 32 points + 4 pad):
+// coordinate k of point r sits at word (k>>2)*kSketchColWords + (k&3)*32 + r.
+constexpr int kSketchColWords = 132;
+
 struct SketchPlanDev {
     int d, m, L, K;
     int Q;            // coordinates per chunk (64 * VPT)
@@ -92,6 +92,8 @@ struct HashOut {
 // Launchers (return cudaError_t of the launch).
 cudaError_t launch_sketch(const SketchPlanDev& plan, const DiscretizeDev& disc, const float* X, int64_t n,
                           int64_t ld, HashOut out, int num_sms, cudaStream_t s);
+cudaError_t launch_sketch_fast(const SketchPlanDev& plan, const DiscretizeDev& disc, const float* X, int64_t n,
+                               int64_t ld, HashOut out, int num_sms, cudaStream_t s);
 size_t sketch_smem_bytes(int Q, int m, int d, int L);
 cudaError_t launch_sketch_chunked(const ChunkedPlanDev& plan, const DiscretizeDev& disc, const float* X, int64_t n,
                                   int64_t ld, HashOut out, int num_sms, cudaStream_t s);
@@ -101,8 +103,6 @@ cudaError_t launch_sketch_hcs(const HcsPlanDev& plan, const DiscretizeDev& disc,
 size_t hcs_smem_bytes(int S, int M12, int m, int nentries, int nst);
 bool hcs_plan_supported(int S, int M12);
 
-cudaError_t launch_dense_gemm_f32(const float* X, int64_t n, int64_t ld, const uint16_t* Rbf16, int m, int d,
-                                  float* Y, cudaStream_t s);
 cudaError_t launch_dense_tc(const float* X, int64_t n, int64_t ld, int d, const uint16_t* R_pad, int m, int d_pad,
                             uint16_t* A_scratch, int64_t rows_per_batch, float* Y, cudaStream_t s,
                             uint64_t* keys = nullptr, int K = 0, const DiscretizeDev* dz = nullptr);
@@ -118,11 +118,12 @@ struct GroupScratch {
     uint32_t* hist;             // [L][nb1][tiles] per-tile L1 digit counts, then their tile scan
     uint32_t* tot;              // [L][nb1] bin totals
     uint32_t* binstart;         // [L][nb1+1]
-    unsigned long long* state;  // [L][chunks] look-back words of the per-chunk kernel
+    unsigned long long* state;  // [L][max(nb1, RLE chunks)] look-back words of the numbering
     uint32_t* perm;             // [L][2n] permutation scratch for bins larger than shared memory
     unsigned long long* vmask;  // [L][2] OR of keys, OR of complemented keys
     void* spec;                 // [2][L] L1 digit specs (group.cu)
-    uint32_t* chunkbin;         // [L][chunks+1] first L1 bin of every L2 chunk
+    uint32_t* biglist;          // [L * nb1] L1 bins larger than the per-unit sort (wide keys)
+    uint32_t* bigcount;         // [1]
     int num_sms;
 };
 struct IndexDev {
@@ -135,7 +136,7 @@ size_t group_tiles(int64_t n);
 int group_bins(int64_t n, int key_width);
 size_t group_hist_words(int64_t n, int key_width);
 size_t group_spec_bytes();
-int group_chunks(int64_t n);
+int group_rle_chunks(int64_t n);
 bool group_is_lsd(int key_width);
 cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_base, int key_width,
                          GroupScratch& sc, IndexDev& out, int* flags, cudaStream_t s);

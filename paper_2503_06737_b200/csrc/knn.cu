@@ -97,15 +97,19 @@ __global__ void __launch_bounds__(kQT) knn_kernel(KnnArgs a, int P) {
     const int64_t qi = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int L = a.L;
-    // 1. bucket sizes of the L tables, prefix in table order
+    // 1. bucket sizes of the L tables, prefix in table order.  Only the first max_cand
+    //    entries are used, so sizes and the prefix saturate at max_cand (no u32 wrap;
+    //    the saturated prefix stays non-decreasing for the search below)
+    const uint32_t cap = (uint32_t)a.max_cand;
     uint32_t carry = 0;
     for (int t0 = 0; t0 < L; t0 += kQT) {
         const int t = t0 + threadIdx.x;
-        const uint32_t c = t < L ? (uint32_t)(a.end[qi * L + t] - a.begin[qi * L + t]) : 0u;
+        const int64_t sz = t < L ? a.end[qi * L + t] - a.begin[qi * L + t] : 0;
+        const uint32_t c = (uint32_t)(sz < (int64_t)cap ? sz : (int64_t)cap);
         uint32_t tot;
-        const uint32_t ex = block_excl(c, ws, &tot);
-        if (t < L) pref[t] = carry + ex;
-        carry += tot;
+        const uint32_t ex = block_excl(c, ws, &tot);   // <= kQT * cap < 2^32
+        if (t < L) pref[t] = min(cap, carry + ex);
+        carry = min(cap, carry + tot);
     }
     if (threadIdx.x == 0) pref[L] = carry;
     __syncthreads();

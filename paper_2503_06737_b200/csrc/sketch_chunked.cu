@@ -188,7 +188,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = ci.t0 + warp; t < ci.t1; t += kWarps) {
             const int lb0 = (t - ci.t0) * K;
             const float* p = T + s_bp[lb0] * 33 + lane;
-            uint64_t f = E2 ? LSHB_FNV_OFFSET : 0ull;
+            uint64_t f = 0;
+            FpKey fk;
             uint32_t sbits = 0;
             float qmax = 0.f;
             auto bin = [&](int kk, uint32_t cnt) {
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const float q = fmaf(acc, cs, s_coff[l]);
                     qmax = fmax_nan_abs_c(qmax, q);
                     z = __float_as_int(__fadd_rd(q, 12582912.0f)) - 0x4B400000;
-                    f = (f ^ (uint64_t)(uint32_t)z) * LSHB_FNV_PRIME;
+                    fk.add((uint32_t)z);
                 } else {
                     z = acc > 0.0f ? 1 : 0;
                     if (KT > 0 && KT <= 32) sbits |= (uint32_t)z << kk;
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (!last) continue;
             if constexpr (E2) {
                 if (!(qmax < 4194304.0f)) {
-                    f = LSHB_FNV_OFFSET;
+                    fk = FpKey();
                     const float* p2 = T + s_bp[lb0] * 33 + lane;
                     for (int kk = 0; kk < K; ++kk) {
                         const int lb = lb0 + kk, l = t * K + kk;
@@ -243,14 +244,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (uint32_t j = 0; j < cnt; ++j) acc += p2[j * 33];
                         p2 += cnt * 33;
                         const int32_t z = floor_code(fmaf(acc, cs, s_coff[l]), dz.flags);
-                        f = (f ^ (uint64_t)(uint32_t)z) * LSHB_FNV_PRIME;
+                        fk.add((uint32_t)z);
                         if (KT == 0 && dbg && valid && out.codes) out.codes[row * m + l] = z;
                     }
                 }
             } else if (KT > 0 && KT <= 32) {
                 f = sbits;
             }
-            if (valid && out.keys) out.keys[(int64_t)t * n + row] = E2 ? fmix64_dev(f) : f;
+            if (valid && out.keys) out.keys[(int64_t)t * n + row] = E2 ? fk.key() : f;
         }
         if (!has_next) break;
         columns_for_chunk(cn);

@@ -210,24 +210,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int tpb = M12 / K;  // tables per block
         if (tid < tpb * 32) {
             const int tb = tid >> 5;
-            uint64_t fp = E2 ? LSHB_FNV_OFFSET : 0ull;
+            uint64_t fp = 0;
+            FpKey fk;
             if (K == 16) {   // the usual K: all 16 codes loaded at once, the chain back to back
                 uint32_t zk[16];
 #pragma unroll
                 for (int kk = 0; kk < 16; ++kk) zk[kk] = zs[(tb * 16 + kk) * 32 + lane];
 #pragma unroll
                 for (int kk = 0; kk < 16; ++kk) {
-                    if constexpr (E2) fp = (fp ^ (uint64_t)zk[kk]) * LSHB_FNV_PRIME;
+                    if constexpr (E2) fk.add(zk[kk]);
                     else fp |= (uint64_t)zk[kk] << kk;
                 }
             } else {
                 for (int kk = 0; kk < K; ++kk) {
                     const uint32_t zc = zs[(tb * K + kk) * 32 + lane];
-                    if constexpr (E2) fp = (fp ^ (uint64_t)zc) * LSHB_FNV_PRIME;
+                    if constexpr (E2) fk.add(zc);
                     else fp |= (uint64_t)zc << kk;
                 }
             }
-            if (valid && out.keys) out.keys[(int64_t)(g * tpb + tb) * n + row] = E2 ? fmix64_dev(fp) : fp;
+            if (valid && out.keys) out.keys[(int64_t)(g * tpb + tb) * n + row] = E2 ? fk.key() : fp;
         }
         return false;
     };

@@ -42,12 +42,15 @@ def build_index_sharded(h: LSH, X_shard, id_base: int, B: int = 12, group=None, 
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
-    idx = h.build_index(X_shard, id_base=id_base, stream=stream)
-    cnt = idx.counts(B, stream=stream)
-    all_counts = torch.empty((world,) + tuple(cnt.shape), dtype=cnt.dtype, device=cnt.device)
-    if world > 1:
-        dist.all_gather_into_tensor(all_counts, cnt.unsqueeze(0).contiguous(), group=group)
-    else:
-        all_counts.copy_(cnt.unsqueeze(0))
-    off = global_offsets(all_counts, rank, stream=stream)
+    s = stream if stream is not None else torch.cuda.current_stream(X_shard.device)
+    # every step below, the collective included, is ordered on `s`
+    with torch.cuda.stream(s):
+        idx = h.build_index(X_shard, id_base=id_base, stream=s)
+        cnt = idx.counts(B, stream=s)
+        all_counts = torch.empty((world,) + tuple(cnt.shape), dtype=cnt.dtype, device=cnt.device)
+        if world > 1:
+            dist.all_gather_into_tensor(all_counts, cnt.unsqueeze(0).contiguous(), group=group)
+        else:
+            all_counts.copy_(cnt.unsqueeze(0))
+        off = global_offsets(all_counts, rank, stream=s)
     return ShardedIndex(idx, id_base, cnt, all_counts, off, B)

@@ -31,3 +31,19 @@ def golden():
             with open(os.path.join(d, name)) as f:
                 out[name[:-5]] = json.load(f)
     return out
+
+
+@pytest.fixture(scope="session")
+def parity_log():
+    """Append one JSON record per parity comparison (exempt counts, fingerprint merges)
+    to $LSH_PARITY_LOG (default gpurun_out/parity_log.jsonl) and echo it to stdout."""
+    import json
+    path = os.environ.get("LSH_PARITY_LOG", os.path.join(ROOT, "gpurun_out", "parity_log.jsonl"))
+    os.makedirs(os.path.dirname(path), exist_ok=True)
+
+    def log(rec: dict):
+        line = json.dumps(rec, sort_keys=True)
+        print("PARITY " + line)
+        with open(path, "a") as f:
+            f.write(line + "\n")
+    return log

@@ -11,6 +11,8 @@
                projection adds its rigorous accumulation bound tc_band_y().
   SRP bits:    bit-exact except entries with |y_ref| < max(1e-6, 6*2^-24*sqrt(k_l)*sigma_l)
                (counted, reported; same derivation).
+  Entries with no nonzero product (an empty sum: exactly 0 in any precision) are
+  never exempt: their bit / code must match exactly.
   keys:        bit-exact for every (table, point) without an exempt coordinate.
   tables:      bit-exact given identical keys.
 """
@@ -93,17 +95,19 @@ def tc_band_y(p: lsh.Params, t: lsh.Tables, X: np.ndarray) -> np.ndarray:
 def code_band(p: lsh.Params, t: lsh.Tables, X: np.ndarray) -> np.ndarray:
     """Per-entry exemption half-width in quotient units (see module docstring)."""
     w = float(np.float32(p.w))
-    derived = 6.0 * FP32_U * np.sqrt(nnz_terms(p, t, X)) * lsh.e2lsh_scale(p) * sigma(p, t, X) / w
+    nnz = nnz_terms(p, t, X)
+    derived = 6.0 * FP32_U * np.sqrt(nnz) * lsh.e2lsh_scale(p) * sigma(p, t, X) / w
     if on_tensor_cores(p):
         derived = np.maximum(derived, tc_band_y(p, t, X) / w)
-    return np.maximum(CODE_BAND, derived)
+    return np.where(nnz > 0, np.maximum(CODE_BAND, derived), 0.0)
 
 
 def srp_band(p: lsh.Params, t: lsh.Tables, X: np.ndarray) -> np.ndarray:
-    derived = 6.0 * FP32_U * np.sqrt(nnz_terms(p, t, X)) * sigma(p, t, X)
+    nnz = nnz_terms(p, t, X)
+    derived = 6.0 * FP32_U * np.sqrt(nnz) * sigma(p, t, X)
     if on_tensor_cores(p):
         derived = np.maximum(derived, tc_band_y(p, t, X))
-    return np.maximum(SRP_BAND, derived)
+    return np.where(nnz > 0, np.maximum(SRP_BAND, derived), 0.0)
 
 
 def exempt_mask(p: lsh.Params, ref: dict) -> np.ndarray:

@@ -32,11 +32,13 @@ for i in range(1 + a.reps):
     if i == 1:
         torch.cuda.synchronize()
         pk.timing_reset()
+        torch.cuda.nvtx.range_push("profile")   # ncu --nvtx --nvtx-include "profile/"
     if a.op == "hash":
         h.hash(X, keys=True, out={"keys": keys})
     else:
         idx = h.build_index(X)
 torch.cuda.synchronize()
+torch.cuda.nvtx.range_pop()
 for k in ("sketch", "group_hist", "group_scan", "group_scatter", "group_sort", "dense_gemm",
           "keys_from_proj"):
     ms, cnt = pk.timing_get(k)
