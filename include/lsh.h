@@ -198,6 +198,20 @@ lsh_status lsh_index_counts(const lsh_index* idx, int32_t B, uint32_t* counts, v
 lsh_status lsh_global_offsets(const uint32_t* all_counts, int32_t G, int32_t rank, int32_t L, int32_t B,
                               int64_t* offsets, void* stream);
 
+/* Cross-shard query (§8(e); "collect the index of all the elements"
+ * hashed to hbar_t(q), over every shard).  Each rank looks its queries up in its own
+ * tables (lsh_query_buckets: local begin/end [nq][L]); the ranges of all ranks are
+ * all-gathered as all_ranges int64 [G][2][M] (device; rank r's begin[M] then end[M],
+ * M = nq*L).  Because the global bucket of (q, t) is the rank-order concatenation of
+ * the ranks' runs (global ids ascend across ranks), rank `rank`'s local entries
+ * ids[begin[j], end[j]) sit at positions
+ *   gbegin[j] = sum_{r < rank} (end_r[j] - begin_r[j])   (int64 [M], device, written)
+ * of that global bucket, whose size is gtotal[j] = sum_r (end_r[j] - begin_r[j])
+ * (int64 [M], device, nullable).  0 <= rank < G, M >= 0 (LSH_EDIM otherwise).
+ * Asynchronous on `stream`. */
+lsh_status lsh_query_global_runs(const int64_t* all_ranges, int32_t G, int32_t rank, int64_t M, int64_t* gbegin,
+                                 int64_t* gtotal, void* stream);
+
 /* ---- parameters, errors, instrumentation -------------------------------- */
 
 typedef enum {

@@ -63,6 +63,7 @@ def lib() -> ctypes.CDLL:
         "lsh_query_knn": (i32, [vp, vp, vp, i64, vp, i64, i64, i32, i32, vp, vp, vp, vp]),
         "lsh_index_counts": (i32, [vp, i32, vp, vp]),
         "lsh_global_offsets": (i32, [vp, i32, i32, i32, i32, vp, vp]),
+        "lsh_query_global_runs": (i32, [vp, i32, i32, i64, vp, vp, vp]),
         "lsh_export_host": (i32, [P(lsh_params), i32, i32, vp, P(sz)]),
         "lsh_get_params": (i32, [vp, i32, i32, vp, P(sz)]),
         "lsh_check": (i32, [vp]),
@@ -156,6 +157,23 @@ def global_offsets(all_counts, rank: int, stream=None):
     _check(lib().lsh_global_offsets(_dev_ptr(all_counts.contiguous(), name="all_counts"), G, rank, L, B,
                                     out.data_ptr(), _stream_ptr(stream)), "lsh_global_offsets")
     return out
+
+
+def query_global_runs(all_ranges, rank: int, stream=None):
+    """lsh_query_global_runs: all_ranges int64 [G, 2, nq, L] (CUDA; every rank's local
+    begin/end) -> (gbegin, gtotal) int64 [nq, L]: where this rank's run sits inside the
+    global (rank-order concatenated) bucket, and that bucket's size."""
+    torch = _torch()
+    if all_ranges.dtype != torch.int64 or all_ranges.dim() != 4 or all_ranges.shape[1] != 2:
+        raise ValueError("all_ranges must be int64 [G, 2, nq, L]")
+    G, _, nq, L = all_ranges.shape
+    gbegin = torch.empty((nq, L), dtype=torch.int64, device=all_ranges.device)
+    gtotal = torch.empty((nq, L), dtype=torch.int64, device=all_ranges.device)
+    M = nq * L
+    _check(lib().lsh_query_global_runs(_dev_ptr(all_ranges.contiguous(), name="all_ranges") if M else None, G, rank,
+                                       M, gbegin.data_ptr() if M else None, gtotal.data_ptr() if M else None,
+                                       _stream_ptr(stream)), "lsh_query_global_runs")
+    return gbegin, gtotal
 
 
 def _torch():

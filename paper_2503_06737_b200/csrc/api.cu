@@ -298,7 +298,7 @@ struct lsh_handle {
     uint32_t* d_binptr = nullptr;
     uint32_t* d_signs = nullptr;
     uint32_t* d_pairs = nullptr;
-    uint32_t* d_bigmask = nullptr;
+    uint32_t* d_fold = nullptr;     // [L+1] fold_ptr, then [nfold] fold entries
     float* d_coff = nullptr;
     uint16_t* d_R = nullptr;
     uint16_t* d_Rpad = nullptr;  // bf16 [m][d_pad], d_pad = roundup(d, 64): tensor-core B operand
@@ -593,7 +593,11 @@ static lsh_status build_plan(lsh_handle* H) {
     }
     const uint32_t ZW = (uint32_t)(Q / 4) * (uint32_t)kSketchColWords;
     int max_cnt = 0;
-    std::vector<uint32_t> pairs(2 * (size_t)m), bigmask(p->L, 0);
+    // per bin: the staged words of its first two coordinates (the zero slot when
+    // missing); its 3rd, 4th, ... coordinates are folded into the first one's word
+    // (fold entries of the bin's table, in bin-sorted order), so the bin's sum is
+    // ((x_1 + x_3) + x_4 + ...) + x_2 — the order the generic path uses too
+    std::vector<uint32_t> pairs(2 * (size_t)m), fold_ptr(p->L + 1, 0), fold;
     for (int l = 0; l < m; ++l) {
         const uint32_t c = bin_ptr[l + 1] - bin_ptr[l];
         max_cnt = std::max(max_cnt, (int)c);
@@ -601,20 +605,24 @@ static lsh_status build_plan(lsh_handle* H) {
         const uint32_t b = c >= 2 ? ent[bin_ptr[l] + 1] : ZW;
         pairs[2 * l] = a * 4u;       // byte offsets inside the staged tile
         pairs[2 * l + 1] = b * 4u;
-        if (c > 2 && p->K <= 32) bigmask[l / p->K] |= 1u << (l % p->K);
+        for (uint32_t j = 2; j < c; ++j) fold.push_back((a << 16) | ent[bin_ptr[l] + j]);
+        fold_ptr[l / p->K + 1] = (uint32_t)fold.size();
     }
+    for (int t = 0; t < p->L; ++t) fold_ptr[t + 1] = std::max(fold_ptr[t + 1], fold_ptr[t]);
+    std::vector<uint32_t> fold_all(fold_ptr.begin(), fold_ptr.end());
+    fold_all.insert(fold_all.end(), fold.begin(), fold.end());
     CK(cudaMalloc(&H->d_entries, sizeof(uint16_t) * std::max(1, d)));
     CK(cudaMalloc(&H->d_binptr, sizeof(uint32_t) * bin_ptr.size()));
     CK(cudaMalloc(&H->d_signs, sizeof(uint32_t) * sign_bits.size()));
     CK(cudaMalloc(&H->d_pairs, sizeof(uint32_t) * 2 * (size_t)m));
-    CK(cudaMalloc(&H->d_bigmask, sizeof(uint32_t) * p->L));
+    CK(cudaMalloc(&H->d_fold, sizeof(uint32_t) * fold_all.size()));
     CK(cudaMemcpy(H->d_entries, ent.data(), sizeof(uint16_t) * d, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(H->d_binptr, bin_ptr.data(), sizeof(uint32_t) * bin_ptr.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(H->d_signs, sign_bits.data(), sizeof(uint32_t) * sign_bits.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(H->d_pairs, pairs.data(), sizeof(uint32_t) * 2 * (size_t)m, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(H->d_bigmask, bigmask.data(), sizeof(uint32_t) * p->L, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(H->d_fold, fold_all.data(), sizeof(uint32_t) * fold_all.size(), cudaMemcpyHostToDevice));
     H->plan = SketchPlanDev{d, m, p->L, p->K, Q, vpt, 1, max_cnt, H->d_entries, H->d_binptr, H->d_signs,
-                            H->d_pairs, H->d_bigmask};
+                            H->d_pairs, H->d_fold, H->d_fold + p->L + 1, (int)fold.size()};
     return LSH_OK;
 }
 
@@ -626,7 +634,7 @@ static void free_handle(lsh_handle* H) {
     cudaFree(H->d_hplan_mem);
     cudaFree(H->d_signs);
     cudaFree(H->d_pairs);
-    cudaFree(H->d_bigmask);
+    cudaFree(H->d_fold);
     cudaFree(H->d_coff);
     cudaFree(H->d_R);
     cudaFree(H->d_Rpad);
@@ -1055,6 +1063,18 @@ extern "C" lsh_status lsh_global_offsets(const uint32_t* all_counts, int32_t G, 
     count_launch();
     timing_end("global_offsets", s);
     if (e != cudaSuccess) return cuda_fail(e, "global_offsets");
+    return LSH_OK;
+}
+
+extern "C" lsh_status lsh_query_global_runs(const int64_t* all_ranges, int32_t G, int32_t rank, int64_t M,
+                                           int64_t* gbegin, int64_t* gtotal, void* stream) {
+    if (G < 1 || rank < 0 || rank >= G || M < 0 || (M > 0 && (!all_ranges || !gbegin))) return LSH_EDIM;
+    cudaStream_t s = (cudaStream_t)stream;
+    timing_begin("query_runs", s);
+    cudaError_t e = launch_query_runs(all_ranges, G, rank, M, gbegin, gtotal, s);
+    if (M > 0) count_launch();
+    timing_end("query_runs", s);
+    if (e != cudaSuccess) return cuda_fail(e, "query_runs");
     return LSH_OK;
 }
 

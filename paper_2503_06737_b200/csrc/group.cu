@@ -1559,5 +1559,31 @@ cudaError_t launch_global_offsets(const uint32_t* all, int G, int rank, int L, i
     return cudaGetLastError();
 }
 
+// Cross-shard query runs: all_ranges int64 [G][2][M] = every rank's local (begin[M],
+// end[M]) of the same M = nq*L (query, table) lookups.  The global bucket of (q, t) is
+// the rank-order concatenation of the ranks' runs, so rank `rank`'s run starts at
+// gbegin[j] = sum_{r < rank} (end_r[j] - begin_r[j]) inside it; gtotal[j] = its size.
+__global__ void __launch_bounds__(256) query_runs_kernel(const int64_t* __restrict__ all, int G, int rank, int64_t M,
+                                                          int64_t* __restrict__ gbegin, int64_t* __restrict__ gtotal) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < M; j += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lower = 0, tot = 0;
+        for (int r = 0; r < G; ++r) {
+            const int64_t sz = all[((int64_t)r * 2 + 1) * M + j] - all[(int64_t)r * 2 * M + j];
+            tot += sz;
+            if (r < rank) lower += sz;
+        }
+        gbegin[j] = lower;
+        if (gtotal) gtotal[j] = tot;
+    }
+}
+
+cudaError_t launch_query_runs(const int64_t* all, int G, int rank, int64_t M, int64_t* gbegin, int64_t* gtotal,
+                              cudaStream_t s) {
+    if (M == 0) return cudaSuccess;
+    const int64_t blocks = (M + 255) / 256;
+    query_runs_kernel<<<(unsigned)(blocks < 4096 ? blocks : 4096), 256, 0, s>>>(all, G, rank, M, gbegin, gtotal);
+    return cudaGetLastError();
+}
+
 }  // namespace lshb
 

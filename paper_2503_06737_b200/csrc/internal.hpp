@@ -29,7 +29,10 @@ struct SketchPlanDev {
     const uint32_t* sign_bits;  // [ceil(d/32)] bit j set = sign(j) = -1 (applied while staging)
     const uint32_t* pairs;      // [2m] per bin: byte offsets (in the staged tile) of its first two coordinates,
                                 //     lo 16 bits / hi 16 bits; missing ones point at the zero slot Q
-    const uint32_t* bigmask;    // [L] bit k set: bin k of table t has more than 2 coordinates
+    const uint32_t* fold_ptr;   // [L+1] table t's fold entries are fold[fold_ptr[t] .. fold_ptr[t+1])
+    const uint32_t* fold;       // [nfold] (dst word << 16) | src word: the 3rd, 4th, ... coordinate of a bin is
+                                //     added into its first coordinate's staged word before the pair gather
+    int nfold;
 };
 
 // Chunked plan (sketch_chunked.cu): tables in groups, per group the coordinates
@@ -147,6 +150,8 @@ cudaError_t launch_knn(const IndexDev& idx, int64_t n, int L, uint32_t id_base, 
                        int64_t nq, int k, int max_cand, int cosine, int64_t* out_ids, float* out_score,
                        int32_t* out_ncand, cudaStream_t s);
 cudaError_t launch_global_offsets(const uint32_t* all, int G, int rank, int L, int B, int64_t* off, cudaStream_t s);
+cudaError_t launch_query_runs(const int64_t* all, int G, int rank, int64_t M, int64_t* gbegin, int64_t* gtotal,
+                              cudaStream_t s);
 cudaError_t launch_counts(const IndexDev& idx, int64_t n, int L, int width, int B, uint32_t* counts,
                           cudaStream_t s);
 

@@ -69,9 +69,9 @@ __device__ __forceinline__ float fmax_nan_abs(float a, float q) {
 //   cnt  [m]   u8           (unused by the kernel body; kept for the layout's users)
 //   ent  [d]   u16          T word offset of the coordinate at each bin-sorted index
 //   sgn  [ceil(d/32)] u32   bit j set: sign(j) = -1
-//   big  [L]   u32          bit k: bin k of table t has more than two coordinates
+//   fold [L+1+d] u32        fold_ptr[L+1], then the fold entries (dst word << 16 | src word)
 struct SketchSmem {
-    size_t t, bp, cnt, ent, coff, sgn, pairs, big, total;
+    size_t t, bp, cnt, ent, coff, sgn, pairs, fold, total;
 };
 __host__ __device__ inline SketchSmem sketch_smem_layout(int Q, int m, int d, int L) {
     SketchSmem o{};
@@ -94,8 +94,8 @@ __host__ __device__ inline SketchSmem sketch_smem_layout(int Q, int m, int d, in
     x += ((size_t)d * 2 + 15) / 16 * 16;
     o.sgn = x;
     x += (size_t)((d + 31) / 32) * 4;
-    o.big = x;
-    x += (size_t)L * 4;
+    o.fold = x;
+    x += (size_t)(L + 1 + d) * 4;   // at most d - 2 fold entries
     o.total = (x + 15) / 16 * 16;
     return o;
 }
@@ -124,7 +124,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* s_coff = reinterpret_cast<float*>(smem_raw + so.coff);
     uint32_t* s_sgn = reinterpret_cast<uint32_t*>(smem_raw + so.sgn);
     uint32_t* s_pairs = reinterpret_cast<uint32_t*>(smem_raw + so.pairs);
-    uint32_t* s_big = reinterpret_cast<uint32_t*>(smem_raw + so.big);
+    uint32_t* s_fptr = reinterpret_cast<uint32_t*>(smem_raw + so.fold);
+    uint32_t* s_fold = s_fptr + L + 1;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t ntiles = (n + 31) >> 5;
@@ -139,7 +140,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = tid; i < d; i += kThreads) s_ent[i] = __ldg(plan.pos + i);
     for (int i = tid; i < (d + 31) / 32; i += kThreads) s_sgn[i] = __ldg(plan.sign_bits + i);
-    for (int i = tid; i < L; i += kThreads) s_big[i] = __ldg(plan.bigmask + i);
+    for (int i = tid; i <= L; i += kThreads) s_fptr[i] = __ldg(plan.fold_ptr + i);
+    for (int i = tid; i < plan.nfold; i += kThreads) s_fold[i] = __ldg(plan.fold + i);
     for (int i = tid; i < 64; i += kThreads) T[ZW + i] = 0.f;
     __syncthreads();
 
@@ -222,7 +224,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     load(tile);
     const float cs = dz.c_scale;
-    const float* Tl = T + lane;
+    float* const Tw = T + lane;   // this lane's (point's) column of the staged tile
+    const float* Tl = Tw;
     while (true) {
         __syncthreads();  // previous gathers finished with T
         store();
@@ -233,12 +236,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t row = tile * 32 + lane;
         const bool valid = row < n;
         if constexpr (KT > 0) {
-            // hot path: each bin's first two coordinates through `pairs` (branch-free; a
-            // missing one reads the zero slot), rare fix-ups for fuller bins, then
-            // discretise + key for the K bins of the table.  Two tables per iteration.
+            // hot path: the 3rd, 4th, ... coordinates of a bin are first folded into its
+            // first coordinate's staged word (this lane's own column: no other lane or warp
+            // reads it — a coordinate belongs to one bin, a bin to one table, a table to one
+            // warp); then every bin is the sum of two staged words through `pairs`
+            // (branch-free; a missing one reads the zero slot).  Two tables per iteration.
 #pragma unroll 2
             for (int t = warp; t < L; t += kWarps) {
                 float acc[KT];
+                {
+                    const uint32_t f1 = s_fptr[t + 1];
+#pragma unroll 1
+                    for (uint32_t f = s_fptr[t]; f < f1; ++f) {
+                        const uint32_t e = s_fold[f];
+                        Tw[e >> 16] += Tw[e & 0xffffu];
+                    }
+                }
                 {
                     // two byte offsets per bin, 2 bins per 128-bit load; one add each
                     const uint4* pp4 = reinterpret_cast<const uint4*>(s_pairs + t * KT * 2);
@@ -249,17 +262,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                         acc[2 * i] = *reinterpret_cast<const float*>(Tb + v.x) + *reinterpret_cast<const float*>(Tb + v.y);
                         acc[2 * i + 1] =
                             *reinterpret_cast<const float*>(Tb + v.z) + *reinterpret_cast<const float*>(Tb + v.w);
-                    }
-                }
-                const uint32_t big = s_big[t];
-                if (big) {
-#pragma unroll
-                    for (int kk = 0; kk < KT; ++kk) {
-                        if ((big >> kk) & 1u) {
-                            const int l = t * KT + kk;
-#pragma unroll 1
-                            for (uint32_t j = s_bp[l] + 2; j < s_bp[l + 1]; ++j) acc[kk] += Tl[s_ent[j]];
-                        }
                     }
                 }
                 uint64_t f;
@@ -306,8 +308,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 FpKey fk;
                 for (int kk = 0; kk < K; ++kk) {
                     const int l = t * K + kk;
+                    // ((x_1 + x_3) + x_4 + ...) + x_2 in bin-sorted order: the fast path's fold order
+                    const uint32_t j0 = s_bp[l], j1 = s_bp[l + 1];
                     float acc = 0.0f;
-                    for (uint32_t j = s_bp[l]; j < s_bp[l + 1]; ++j) acc += Tl[s_ent[j]];
+                    if (j1 > j0) acc += Tl[s_ent[j0]];
+                    for (uint32_t j = j0 + 2; j < j1; ++j) acc += Tl[s_ent[j]];
+                    if (j1 > j0 + 1) acc += Tl[s_ent[j0 + 1]];
                     int32_t z;
                     if constexpr (E2) {
                         z = floor_code(fmaf(acc, cs, s_coff[l]), dz.flags);

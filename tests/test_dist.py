@@ -126,3 +126,35 @@ def test_global_offsets_oracle_properties():
             assert start == pos
             pos += ln
         assert pos == allc[:, t].sum()
+
+
+def _gather_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2503_06737_b200.dist import all_gather_device
+        x = torch.arange(12, dtype=torch.int64).reshape(2, 6) + 100 * rank
+        out = all_gather_device(x)
+        q.put((rank, out.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_all_gather_device_gloo_world2():
+    """The product's backend-agnostic gather (dist.all_gather_device) under gloo: [G, *shape]
+    in rank order on every rank (the host path the GPU world-2 test uses)."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    want = np.stack([np.arange(12).reshape(2, 6) + 100 * r for r in range(world)])
+    for r in range(world):
+        assert np.array_equal(res[r], want)

@@ -14,7 +14,7 @@ done
 python tools/summarize_r2.py $P C4:CS_E2LSH=/tmp/C4_CS_E2LSH_full.ncu-rep C4:CS_SRP=/tmp/C4_CS_SRP_full.ncu-rep \
     C5:HCS_E2LSH=/tmp/C5_HCS_E2LSH_full.ncu-rep > $P/summarize.log 2>&1
 # per-line source view of the two C4 E2LSH hot kernels
-for K in sketch_kernel g2w g1_scatter; do
+for K in sketch_kernel g2a g2e g1_scatter; do
   ncu -i /tmp/C4_CS_E2LSH_full.ncu-rep --page source --csv -k regex:$K > $P/src_${K}.csv 2>/dev/null
 done
 ls -la $P | head -30
