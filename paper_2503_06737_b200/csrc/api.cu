@@ -870,7 +870,7 @@ static lsh_status group_impl(const lsh_handle* H, const uint64_t* keys, uint64_t
     const size_t b_perm = own_perm ? b_keys : 0;
     const size_t b_vm = sizeof(unsigned long long) * 2 * (size_t)L;
     const size_t b_spec = group_spec_bytes() * 2 * (size_t)L;
-    const size_t b_cb = sizeof(uint32_t) * ((size_t)L * nb1 + 1);
+    const size_t b_cb = sizeof(uint32_t) * ((size_t)L * nb1 + 2);   // big-bin count, g2a ticket, big-bin list
     void* mem = nullptr;
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
     const size_t total = al(b_keys) + al(b_ids) + al(b_hist) + al(b_tot) + al(b_bs) + al(b_st) + al(b_perm) + al(b_vm) +
@@ -893,7 +893,7 @@ static lsh_status group_impl(const lsh_handle* H, const uint64_t* keys, uint64_t
         sc.vmask = (unsigned long long*)take(b_vm);
         sc.spec = take(b_spec);
         sc.bigcount = (uint32_t*)take(b_cb);
-        sc.biglist = sc.bigcount + 1;
+        sc.biglist = sc.bigcount + 2;
     }
     sc.num_sms = H->num_sms;
     cudaError_t e = launch_group(keys, n, L, (uint32_t)id_base, H->key_width, sc, I->dev, H->d_flags, s);

@@ -553,8 +553,8 @@ struct G2Args {
     uint32_t id_base;           // ids of a table are id_base + row
     const uint32_t* biglist;    // t * nb1 + bin of every bin larger than kG2BinCap
     const uint32_t* bigcount;   // [1] entries of biglist
-    uint32_t* binheads;         // [L][nb1] buckets per bin
-    uint32_t* binbase;          // [L][nb1] bucket number of each bin's first bucket
+    uint32_t* binheads;         // [L][nb1] buckets per bin (big bins: written by g2_big)
+    uint32_t* ticket;           // [1] g2a's dynamic bin counter (zero before the launch)
     IndexDev out;
 };
 
@@ -872,7 +872,7 @@ __device__ void big_bin_sort(const G2Args& a, int t, int64_t lo, int64_t len, un
 }
 
 // Big bins: sort (permutation in p0), write the bin's ids in final order and its
-// bucket count; g2e emits its ukeys / offs through the permutation.  Persistent over
+// bucket count; g2a emits its ukeys / offs through the permutation.  Persistent over
 // the big-bin list.
 __global__ void __launch_bounds__(kG2Threads) g2_big(G2Args a) {
     extern __shared__ __align__(16) unsigned char g2_dsm[];
@@ -918,9 +918,10 @@ __global__ void __launch_bounds__(kG2Threads) g2_big(G2Args a) {
 //       members by (key, id), and segments longer than kG2aLong (duplicate-heavy
 //       codes) are bitonic-sorted; a bucket head is an item with no equal key of
 //       smaller id;
-//   (3) ids and the sorted keys stream out coalesced (keys in place, over the bin's
-//       L1 output), plus the bin's bucket count.
-// g2s scans the counts per table, g2e numbers the buckets from the sorted keys.
+//   (3) ids stream out coalesced;
+//   (4) the bin's bucket count is published for a decoupled look-back over the bins of
+//       its table (dynamic ticket order); warp 0 looks back while the others write
+//       the ids, then ukeys / offs are written at their final, compacted positions.
 // ---------------------------------------------------------------------------
 constexpr int kG2aT = 128;
 constexpr int kG2aW = kG2aT / 32;
@@ -976,17 +977,63 @@ __device__ void g2a_long_segment(G2aSmem& S, uint32_t s0, uint32_t len, uint16_t
     __syncthreads();
 }
 
+// Big bin (sorted by g2_big: ids written, permutation in a.scratch, bucket count in
+// binheads): publish, look back, emit its ukeys / offs through the permutation.
+__device__ void g2a_big_emit(const G2Args& a, int t, int bin, int64_t lo, int len, uint32_t* s_base) {
+    __shared__ uint32_t ws[kG2aW];
+    const int nb1 = a.nb1;
+    const int64_t n = a.n;
+    const uint32_t agg = a.binheads[(int64_t)t * nb1 + bin];
+    unsigned long long* st = a.state + (int64_t)t * nb1;
+    if (threadIdx.x < 32) {
+        const uint32_t pre = chained_prefix_warp(st, bin, agg);
+        if (threadIdx.x == 0) *s_base = pre;
+    }
+    __syncthreads();
+    uint32_t b = *s_base;
+    const uint64_t* gk = a.keys + (int64_t)t * n + lo;
+    const uint32_t* perm = a.scratch + (int64_t)t * 2 * n + lo;
+    uint64_t* uk = a.out.ukeys + (int64_t)t * n;
+    uint32_t* of = a.out.offs + (int64_t)t * (n + 1);
+    for (int p0 = 0; p0 < len; p0 += kG2aT) {
+        const int p = p0 + (int)threadIdx.x;
+        const uint64_t k = p < len ? gk[perm[p]] : 0ull;
+        const bool h = p < len && (p == 0 || k != gk[perm[p - 1]]);
+        uint32_t all;
+        const uint32_t ex = block_excl_scan<kG2aT>(h ? 1u : 0u, ws, &all);
+        if (h) {
+            uk[b + ex] = k;
+            of[b + ex] = (uint32_t)(lo + p);
+        }
+        b += all;
+    }
+    if (bin == nb1 - 1 && threadIdx.x == 0) {
+        a.out.nb[t] = b;
+        of[b] = (uint32_t)n;
+    }
+}
+
 __global__ void __launch_bounds__(kG2aT) g2a(G2Args a) {
     extern __shared__ __align__(16) unsigned char g2a_dsm[];
     G2aSmem& S = *reinterpret_cast<G2aSmem*>(g2a_dsm);
+    __shared__ uint32_t s_tick, s_base;
     const int u = threadIdx.x, lane = u & 31, wu = u >> 5;
     const int nb1 = a.nb1;
     const int64_t n = a.n;
-    const int t = (int)(blockIdx.x / nb1), bin = (int)(blockIdx.x % nb1);   // table-major
+    // bins are numbered through a dynamic ticket, so every bin this CTA
+    // looks back at belongs to a CTA that is already running: the look-back cannot stall
+    if (u == 0) s_tick = atomicAdd(a.ticket, 1u);
+    __syncthreads();
+    // tables interleaved: the CTAs in flight cover ~1/L of every table's bins, so each
+    // table's look-back chain only has to advance a few bins per CTA lifetime
+    const int t = (int)(s_tick % (uint32_t)a.L), bin = (int)(s_tick / (uint32_t)a.L);
     const uint32_t* bs = a.binstart + (int64_t)t * (nb1 + 1);
     const int64_t lo = bs[bin];
     const int len = (int)((int64_t)bs[bin + 1] - lo);
-    if (len > kG2aCap) return;   // g2_big's
+    if (len > kG2aCap) {
+        g2a_big_emit(a, t, bin, lo, len, &s_base);
+        return;
+    }
     uint64_t* gk = const_cast<uint64_t*>(a.keys) + (int64_t)t * n + lo;
     const uint32_t* gi = a.ids + (int64_t)t * n + lo;
     uint64_t kr[kG2aIPT];
@@ -1132,7 +1179,10 @@ __global__ void __launch_bounds__(kG2aT) g2a(G2Args a) {
     }
     heads = __reduce_add_sync(0xffffffffu, heads);
     if (lane == 0) atomicAdd(&S.heads, heads);
-    __syncthreads();   // every read of the digit regions is done
+    __syncthreads();   // every read of the digit regions is done; S.heads complete
+    unsigned long long* st = a.state + (int64_t)t * nb1;
+    const uint32_t agg = S.heads;
+    if (u == 0) st_release(st + bin, ((bin == 0 ? 2ull : 1ull) << 32) | agg);   // publish early
 #pragma unroll
     for (int j = 0; j < kG2aIPT; ++j) {
         const int i = u + j * kG2aT;
@@ -1142,89 +1192,43 @@ __global__ void __launch_bounds__(kG2aT) g2a(G2Args a) {
         }
     }
     __syncthreads();
-    // (3) ids and sorted keys out (coalesced; keys in place over the bin's L1 output)
+    // (3) ids out (coalesced) while warp 0 looks back for the bin's first bucket number
     uint32_t* od = a.out.ids + (int64_t)t * n + lo;
-    for (int p = u; p < len; p += kG2aT) {
-        od[p] = S.si[p];
-        __stcs(gk + p, S.sk[p]);
+    for (int p = u; p < len; p += kG2aT) __stcs(od + p, S.si[p]);
+    if (u < 32) {
+        const uint32_t pre = chained_prefix_warp(st, bin, agg, /*published=*/true);
+        if (u == 0) s_base = pre;
     }
-    if (u == 0) a.binheads[(int64_t)t * nb1 + bin] = S.heads;
-}
-
-// g2s: per table, bucket base of every bin = exclusive scan of the bins' bucket
-// counts; nb[t] and the closing offs[nb] = n.
-__global__ void __launch_bounds__(1024) g2s(G2Args a) {
-    __shared__ uint32_t ws[32];
-    const int t = blockIdx.x, nb1 = a.nb1;
-    const uint32_t* hc = a.binheads + (int64_t)t * nb1;
-    uint32_t* bb = a.binbase + (int64_t)t * nb1;
-    constexpr int PT = 2;   // nb1 <= 2048
-    uint32_t v[PT], s = 0;
-#pragma unroll
-    for (int j = 0; j < PT; ++j) {
-        const int b = threadIdx.x * PT + j;
-        v[j] = b < nb1 ? hc[b] : 0u;
-        s += v[j];
-    }
-    uint32_t tot;
-    uint32_t ex = block_excl_scan<1024>(s, ws, &tot);
-#pragma unroll
-    for (int j = 0; j < PT; ++j) {
-        const int b = threadIdx.x * PT + j;
-        if (b < nb1) bb[b] = ex;
-        ex += v[j];
-    }
-    if (threadIdx.x == 0) {
-        a.out.nb[t] = tot;
-        a.out.offs[(int64_t)t * (a.n + 1) + tot] = (uint32_t)a.n;
-    }
-}
-
-// g2e: bucket numbering of one bin from its sorted keys: a head is a key that differs
-// from its predecessor (the first key of a bin always does: bins differ in the L1
-// digit); ukeys[base + #heads before] = key, offs[...] = its position.  Big bins read
-// their keys through g2_big's permutation.
-constexpr int kG2eT = 256;
-__global__ void __launch_bounds__(kG2eT) g2e(G2Args a) {
-    __shared__ uint32_t wc[kG2eT / 32];
-    const int u = threadIdx.x, lane = u & 31, wu = u >> 5;
-    const int nb1 = a.nb1;
-    const int64_t n = a.n;
-    const int t = (int)(blockIdx.x / nb1), bin = (int)(blockIdx.x % nb1);
-    const uint32_t* bs = a.binstart + (int64_t)t * (nb1 + 1);
-    const int64_t lo = bs[bin];
-    const int len = (int)((int64_t)bs[bin + 1] - lo);
-    if (len == 0) return;
-    const uint64_t* gk = a.keys + (int64_t)t * n + lo;
-    const uint32_t* perm = len > kG2aCap ? a.scratch + (int64_t)t * 2 * n + lo : nullptr;
-    auto key = [&](int p) { return perm ? gk[perm[p]] : __ldcs(gk + p); };
-    uint32_t b = a.binbase[(int64_t)t * nb1 + bin];
+    __syncthreads();
+    // (4) ukeys / offs: a head is a key that differs from its predecessor (the first key
+    // of a bin always does: bins differ in the L1 digit)
+    const uint32_t base = s_base;
     uint64_t* uk = a.out.ukeys + (int64_t)t * n;
     uint32_t* of = a.out.offs + (int64_t)t * (n + 1);
-    for (int p0 = 0; p0 < len; p0 += kG2eT) {
-        const int p = p0 + u;
-        const bool v = p < len;
-        const uint64_t k = v ? key(p) : 0ull;
-        uint64_t kp = __shfl_up_sync(0xffffffffu, k, 1);
-        if (lane == 0 && p > 0 && v) kp = key(p - 1);
-        const bool h = v && (p == 0 || k != kp);
-        const uint32_t m = __ballot_sync(0xffffffffu, h);
-        if (lane == 0) wc[wu] = __popc(m);
-        __syncthreads();
-        uint32_t before = 0, all = 0;
-#pragma unroll
-        for (int w = 0; w < kG2eT / 32; ++w) {
-            const uint32_t c = wc[w];
-            before += w < wu ? c : 0u;
-            all += c;
+    if (agg == (uint32_t)len) {
+        // every key distinct (the common case for fingerprints): bucket p = item p
+        for (int p = u; p < len; p += kG2aT) {
+            __stcs(uk + base + p, S.sk[p]);
+            __stcs(of + base + p, (uint32_t)(lo + p));
         }
-        if (h) {
-            const uint32_t bb = b + before + __popc(m & lanemask_lt());
-            uk[bb] = k;
-            of[bb] = (uint32_t)(lo + p);
+    } else {
+        uint32_t b = base;
+        for (int p0 = 0; p0 < len; p0 += kG2aT) {
+            const int p = p0 + u;
+            const uint64_t k = p < len ? S.sk[p] : 0ull;
+            const bool h = p < len && (p == 0 || k != S.sk[p - 1]);
+            uint32_t all;
+            const uint32_t ex = block_excl_scan<kG2aT>(h ? 1u : 0u, S.ws, &all);
+            if (h) {
+                __stcs(uk + b + ex, k);
+                __stcs(of + b + ex, (uint32_t)(lo + p));
+            }
+            b += all;
         }
-        b += all;
-        __syncthreads();
+    }
+    if (bin == nb1 - 1 && u == 0) {
+        a.out.nb[t] = base + agg;
+        of[base + agg] = (uint32_t)n;
     }
 }
 
@@ -1387,7 +1391,9 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
         timing_end("group_sort", s);
         return cudaGetLastError();
     }
-    e = cudaMemsetAsync(sc.bigcount, 0, sizeof(uint32_t), s);
+    e = cudaMemsetAsync(sc.bigcount, 0, 2 * sizeof(uint32_t), s);   // big-bin count, g2a ticket
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(sc.state, 0, sizeof(unsigned long long) * (size_t)L * nb1, s);   // look-back words
     if (e != cudaSuccess) return e;
     e = l1_pass(keys, nullptr, sc.keys_a, sc.ids_a, n, L, spec, nb1, id_base, sc, sc.biglist, sc.bigcount, sc.num_sms, s,
                 true, /*stable=*/false);
@@ -1407,8 +1413,8 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
     a.biglist = sc.biglist;
     a.bigcount = sc.bigcount;
     a.out = out;
-    a.binheads = reinterpret_cast<uint32_t*>(sc.state);
-    a.binbase = a.binheads + (size_t)L * nb1;
+    a.binheads = sc.tot;   // bin totals are dead after g1_binstart
+    a.ticket = sc.bigcount + 1;
     const size_t smb = g2_big_smem();
     e = cudaFuncSetAttribute(g2_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb);
     if (e != cudaSuccess) return e;
@@ -1417,11 +1423,7 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
     const unsigned bins = (unsigned)((int64_t)L * nb1);
     g2_big<<<sc.num_sms, kG2Threads, smb, s>>>(a);   // bins larger than kG2aCap (usually none)
     count_launch();
-    g2a<<<bins, kG2aT, sizeof(G2aSmem), s>>>(a);      // sort every bin, ids + sorted keys out
-    count_launch();
-    g2s<<<L, 1024, 0, s>>>(a);                        // bucket numbers of each bin's first bucket
-    count_launch();
-    g2e<<<bins, kG2eT, 0, s>>>(a);                    // ukeys / offs
+    g2a<<<bins, kG2aT, sizeof(G2aSmem), s>>>(a);      // sort every bin; ids, ukeys, offs out
     count_launch();
     timing_end("group_sort", s);
     return cudaGetLastError();
