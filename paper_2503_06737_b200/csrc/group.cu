@@ -933,6 +933,36 @@ constexpr int kG2aLong = 64;                   // longest segment ranked item by
 constexpr int kG2aLongMax = kG2aCap / kG2aLong;
 static_assert(kG2aCap == kG2BinCap, "big-bin threshold");
 
+// Barrier of the per-bin sort: named barrier 1 over its 128 sorting threads (a
+// persistent variant with a producer warp that never joins it was measured slower:
+// C4 g2 1.25 vs 0.91 ms — fewer CTAs per SM hide less of the sort's own latency).
+__device__ __forceinline__ void cbar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void g_mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(g_smem_u32(bar)) : "memory");
+}
+// Exclusive scan of one value per consumer thread (128), with total.
+__device__ __forceinline__ uint32_t cblock_excl_scan(uint32_t v, uint32_t* ws, uint32_t* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) ws[warp] = x;
+    cbar();
+    uint32_t before = 0, all = 0;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        const uint32_t c = ws[w];
+        before += w < warp ? c : 0u;
+        all += c;
+    }
+    if (total) *total = all;
+    cbar();
+    return before + x - v;
+}
+
 struct __align__(16) G2aSmem {
     uint64_t sk[kG2aCap];
     uint32_t si[kG2aCap];
@@ -948,7 +978,7 @@ __device__ void g2a_long_segment(G2aSmem& S, uint32_t s0, uint32_t len, uint16_t
     int P = 1;
     while (P < (int)len) P <<= 1;
     for (int i = threadIdx.x; i < P; i += kG2aT) perm[i] = (uint16_t)(i < (int)len ? s0 + i : 0xffffu);
-    __syncthreads();
+    cbar();
     auto less = [&](uint16_t x, uint16_t y) {   // pads (0xffff) sort last
         if (x == 0xffffu) return false;
         if (y == 0xffffu) return true;
@@ -966,7 +996,7 @@ __device__ void g2a_long_segment(G2aSmem& S, uint32_t s0, uint32_t len, uint16_t
                     perm[hi] = x;
                 }
             }
-            __syncthreads();
+            cbar();
         }
     }
     for (int j = threadIdx.x; j < (int)len; j += kG2aT) {
@@ -974,7 +1004,7 @@ __device__ void g2a_long_segment(G2aSmem& S, uint32_t s0, uint32_t len, uint16_t
         const bool head = j == 0 || S.sk[perm[j - 1]] != S.sk[pj];
         fin[pj] = (uint16_t)((s0 + j) | (head ? 0x8000u : 0u));
     }
-    __syncthreads();
+    cbar();
 }
 
 // Big bin (sorted by g2_big: ids written, permutation in a.scratch, bucket count in
@@ -989,7 +1019,7 @@ __device__ void g2a_big_emit(const G2Args& a, int t, int bin, int64_t lo, int le
         const uint32_t pre = chained_prefix_warp(st, bin, agg);
         if (threadIdx.x == 0) *s_base = pre;
     }
-    __syncthreads();
+    cbar();
     uint32_t b = *s_base;
     const uint64_t* gk = a.keys + (int64_t)t * n + lo;
     const uint32_t* perm = a.scratch + (int64_t)t * 2 * n + lo;
@@ -1000,7 +1030,7 @@ __device__ void g2a_big_emit(const G2Args& a, int t, int bin, int64_t lo, int le
         const uint64_t k = p < len ? gk[perm[p]] : 0ull;
         const bool h = p < len && (p == 0 || k != gk[perm[p - 1]]);
         uint32_t all;
-        const uint32_t ex = block_excl_scan<kG2aT>(h ? 1u : 0u, ws, &all);
+        const uint32_t ex = cblock_excl_scan(h ? 1u : 0u, ws, &all);
         if (h) {
             uk[b + ex] = k;
             of[b + ex] = (uint32_t)(lo + p);
@@ -1013,37 +1043,24 @@ __device__ void g2a_big_emit(const G2Args& a, int t, int bin, int64_t lo, int le
     }
 }
 
-__global__ void __launch_bounds__(kG2aT) g2a(G2Args a) {
-    extern __shared__ __align__(16) unsigned char g2a_dsm[];
-    G2aSmem& S = *reinterpret_cast<G2aSmem*>(g2a_dsm);
-    __shared__ uint32_t s_tick, s_base;
+// Sort one L1 bin of len <= kG2aCap items (keys src_k[0..len), ids src_i[0..len)) in
+// shared memory and emit its ids, ukeys and offs (module comment above).  Executed by
+// the 128 threads of the CTA (named barrier 1); `release` (nullable): mbarrier arrived
+// on by thread 0 once the items are in registers (a source stage may then be refilled).
+__device__ __forceinline__ void g2_bin(const G2Args& a, G2aSmem& S, int t, int bin, int64_t lo, int len,
+                                       const uint64_t* src_k, const uint32_t* src_i, uint64_t* release,
+                                       uint32_t* s_base_p) {
     const int u = threadIdx.x, lane = u & 31, wu = u >> 5;
     const int nb1 = a.nb1;
     const int64_t n = a.n;
-    // bins are numbered through a dynamic ticket, so every bin this CTA
-    // looks back at belongs to a CTA that is already running: the look-back cannot stall
-    if (u == 0) s_tick = atomicAdd(a.ticket, 1u);
-    __syncthreads();
-    // tables interleaved: the CTAs in flight cover ~1/L of every table's bins, so each
-    // table's look-back chain only has to advance a few bins per CTA lifetime
-    const int t = (int)(s_tick % (uint32_t)a.L), bin = (int)(s_tick / (uint32_t)a.L);
-    const uint32_t* bs = a.binstart + (int64_t)t * (nb1 + 1);
-    const int64_t lo = bs[bin];
-    const int len = (int)((int64_t)bs[bin + 1] - lo);
-    if (len > kG2aCap) {
-        g2a_big_emit(a, t, bin, lo, len, &s_base);
-        return;
-    }
-    uint64_t* gk = const_cast<uint64_t*>(a.keys) + (int64_t)t * n + lo;
-    const uint32_t* gi = a.ids + (int64_t)t * n + lo;
     uint64_t kr[kG2aIPT];
     uint32_t ir[kG2aIPT], dr[kG2aIPT];
 #pragma unroll
     for (int j = 0; j < kG2aIPT; ++j) {
         const int i = u + j * kG2aT;
         if (i < len) {
-            kr[j] = __ldcs(gk + i);
-            ir[j] = __ldcs(gi + i);
+            kr[j] = src_k[i];
+            ir[j] = src_i[i];
         }
     }
     {
@@ -1059,7 +1076,8 @@ __global__ void __launch_bounds__(kG2aT) g2a(G2Args a) {
     const int hb = sp.below == 0 ? 0 : 64 - __clzll((long long)sp.below);
     const int D = min(kG2aD, hb), sh = hb - D;
     const uint32_t dmask = (1u << D) - 1u;
-    __syncthreads();
+    cbar();
+    if (release && u == 0) g_mbar_arrive(release);   // the stage is free for the next bin
     // (1) digit counts; the atomic's old value is the item's rank inside its digit
 #pragma unroll
     for (int j = 0; j < kG2aIPT; ++j) {
@@ -1071,7 +1089,7 @@ __global__ void __launch_bounds__(kG2aT) g2a(G2Args a) {
             dr[j] = (d << 16) | ((old >> hs) & 0xffffu);
         }
     }
-    __syncthreads();
+    cbar();
     {
         // exclusive scan of the 4096 counters: thread u owns words [16u, 16u + 16)
         constexpr int WPT = kG2aCW / kG2aT;
@@ -1094,7 +1112,7 @@ __global__ void __launch_bounds__(kG2aT) g2a(G2Args a) {
             if (lane >= o) x += y;
         }
         if (lane == 31) S.ws[wu] = x;
-        __syncthreads();
+        cbar();
         uint32_t ex = x - sum;
 #pragma unroll
         for (int w = 0; w < kG2aW; ++w) ex += w < wu ? S.ws[w] : 0u;
@@ -1111,7 +1129,7 @@ __global__ void __launch_bounds__(kG2aT) g2a(G2Args a) {
             o4[q4] = make_uint4(o[0], o[1], o[2], o[3]);
         }
     }
-    __syncthreads();
+    cbar();
     // (2) place: an item alone in its digit is final; the others go to their digit's
     // region (arbitrary order) and are ranked below.  dr: kDone, or (s0 << 16) | len
     // for a short segment, or kLong | position for a long one
@@ -1140,7 +1158,7 @@ __global__ void __launch_bounds__(kG2aT) g2a(G2Args a) {
             }
         }
     }
-    __syncthreads();
+    cbar();
     // rank inside shared digits by (key, id); f = final position
 #pragma unroll
     for (int j = 0; j < kG2aIPT; ++j) {
@@ -1179,7 +1197,7 @@ __global__ void __launch_bounds__(kG2aT) g2a(G2Args a) {
     }
     heads = __reduce_add_sync(0xffffffffu, heads);
     if (lane == 0) atomicAdd(&S.heads, heads);
-    __syncthreads();   // every read of the digit regions is done; S.heads complete
+    cbar();   // every read of the digit regions is done; S.heads complete
     unsigned long long* st = a.state + (int64_t)t * nb1;
     const uint32_t agg = S.heads;
     if (u == 0) st_release(st + bin, ((bin == 0 ? 2ull : 1ull) << 32) | agg);   // publish early
@@ -1191,18 +1209,18 @@ __global__ void __launch_bounds__(kG2aT) g2a(G2Args a) {
             S.si[dr[j]] = ir[j];
         }
     }
-    __syncthreads();
+    cbar();
     // (3) ids out (coalesced) while warp 0 looks back for the bin's first bucket number
     uint32_t* od = a.out.ids + (int64_t)t * n + lo;
     for (int p = u; p < len; p += kG2aT) __stcs(od + p, S.si[p]);
     if (u < 32) {
         const uint32_t pre = chained_prefix_warp(st, bin, agg, /*published=*/true);
-        if (u == 0) s_base = pre;
+        if (u == 0) *s_base_p = pre;
     }
-    __syncthreads();
+    cbar();
     // (4) ukeys / offs: a head is a key that differs from its predecessor (the first key
     // of a bin always does: bins differ in the L1 digit)
-    const uint32_t base = s_base;
+    const uint32_t base = *s_base_p;
     uint64_t* uk = a.out.ukeys + (int64_t)t * n;
     uint32_t* of = a.out.offs + (int64_t)t * (n + 1);
     if (agg == (uint32_t)len) {
@@ -1218,7 +1236,7 @@ __global__ void __launch_bounds__(kG2aT) g2a(G2Args a) {
             const uint64_t k = p < len ? S.sk[p] : 0ull;
             const bool h = p < len && (p == 0 || k != S.sk[p - 1]);
             uint32_t all;
-            const uint32_t ex = block_excl_scan<kG2aT>(h ? 1u : 0u, S.ws, &all);
+            const uint32_t ex = cblock_excl_scan(h ? 1u : 0u, S.ws, &all);
             if (h) {
                 __stcs(uk + b + ex, k);
                 __stcs(of + b + ex, (uint32_t)(lo + p));
@@ -1230,6 +1248,30 @@ __global__ void __launch_bounds__(kG2aT) g2a(G2Args a) {
         a.out.nb[t] = base + agg;
         of[base + agg] = (uint32_t)n;
     }
+}
+
+
+__global__ void __launch_bounds__(kG2aT) g2a(G2Args a) {
+    extern __shared__ __align__(16) unsigned char g2a_dsm[];
+    G2aSmem& S = *reinterpret_cast<G2aSmem*>(g2a_dsm);
+    __shared__ uint32_t s_tick, s_base;
+    const int nb1 = a.nb1;
+    const int64_t n = a.n;
+    // bins are numbered through a dynamic ticket, so every bin this CTA looks back at
+    // belongs to a CTA that is already running: the look-back cannot stall
+    if (threadIdx.x == 0) s_tick = atomicAdd(a.ticket, 1u);
+    cbar();
+    // tables interleaved: the CTAs in flight cover ~1/L of every table's bins, so each
+    // table's look-back chain only has to advance a few bins per CTA lifetime
+    const int t = (int)(s_tick % (uint32_t)a.L), bin = (int)(s_tick / (uint32_t)a.L);
+    const uint32_t* bs = a.binstart + (int64_t)t * (nb1 + 1);
+    const int64_t lo = bs[bin];
+    const int len = (int)((int64_t)bs[bin + 1] - lo);
+    if (len > kG2aCap) {
+        g2a_big_emit(a, t, bin, lo, len, &s_base);
+        return;
+    }
+    g2_bin(a, S, t, bin, lo, len, a.keys + (int64_t)t * n + lo, a.ids + (int64_t)t * n + lo, nullptr, &s_base);
 }
 
 // Run-length encoding of fully sorted keys (LSD path): chunk c = items
@@ -1423,7 +1465,7 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
     const unsigned bins = (unsigned)((int64_t)L * nb1);
     g2_big<<<sc.num_sms, kG2Threads, smb, s>>>(a);   // bins larger than kG2aCap (usually none)
     count_launch();
-    g2a<<<bins, kG2aT, sizeof(G2aSmem), s>>>(a);      // sort every bin; ids, ukeys, offs out
+    g2a<<<bins, kG2aT, sizeof(G2aSmem), s>>>(a);   // sort every bin; ids, ukeys, offs out
     count_launch();
     timing_end("group_sort", s);
     return cudaGetLastError();
