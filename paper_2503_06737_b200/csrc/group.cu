@@ -1251,7 +1251,7 @@ __device__ __forceinline__ void g2_bin(const G2Args& a, G2aSmem& S, int t, int b
 }
 
 
-__global__ void __launch_bounds__(kG2aT) g2a(G2Args a) {
+__global__ void __launch_bounds__(kG2aT, 6) g2a(G2Args a) {
     extern __shared__ __align__(16) unsigned char g2a_dsm[];
     G2aSmem& S = *reinterpret_cast<G2aSmem*>(g2a_dsm);
     __shared__ uint32_t s_tick, s_base;
