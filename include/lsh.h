@@ -246,7 +246,7 @@ uint64_t lsh_launch_count(void);
 void lsh_timing_enable(int32_t on);
 /* Names: "sketch", "sketch_query", "dense_gemm", "dense_gemm_query", "keys_from_proj",
  * "group_hist", "group_scan", "group_scatter", "group_sort", "lookup", "knn", "counts",
- * "global_offsets".  Synchronises the device.
+ * "global_offsets", "query_runs".  Synchronises the device.
  * Returns accumulated milliseconds and launch count since the last reset. */
 lsh_status lsh_timing_get(const char* name, double* ms, int64_t* launches);
 void lsh_timing_reset(void);

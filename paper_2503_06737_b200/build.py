@@ -37,8 +37,9 @@ def _stale() -> bool:
 
 
 def build(verbose: bool = False, force: bool = False, variant: str = "") -> str:
-    """variant "prof": diagnostic library liblsh_b200_prof.so (-DLSHB_PROF: per-phase
-    clock counters); never loaded by the product path."""
+    """variant "checked": liblsh_b200_checked.so (-DLSHB_CHECKS: device-side bounds
+    checks on every index write, reported as "LSHB_DCHECK file:line"), loaded instead of
+    the product library when LSH_LIB_VARIANT=checked (tools/gpu_checked.sh)."""
     target = OUT if not variant else OUT.replace(".so", f"_{variant}.so")
     if not variant and not force and not _stale():
         return OUT
@@ -49,8 +50,8 @@ def build(verbose: bool = False, force: bool = False, variant: str = "") -> str:
                     "-I" + os.path.join(HERE, "..", "include")]
     if verbose:
         flags += ["-Xptxas", "-v"]
-    if variant == "prof":
-        flags += ["-DLSHB_PROF"]
+    if variant == "checked":
+        flags += ["-DLSHB_CHECKS"]
     procs = []
     for src in SOURCES:
         obj = os.path.join(tmp, src.replace(".cu", ".o"))

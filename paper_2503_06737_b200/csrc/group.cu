@@ -531,8 +531,10 @@ __global__ void __launch_bounds__(kSThreads, 1)
         for (int p = threadIdx.x; p < cnt; p += kSThreads) {
             const uint32_t i = sp[p], dg = sd[p];
             const uint32_t pos = gpos[dg] + ((uint32_t)p - loc[dg]);
-            kout[tb + pos] = kr[i];
-            iout[tb + pos] = IMPLICIT_IDS ? id_base + (uint32_t)(tile * kG1Tile) + i : __ldg(ir + i);
+            if (LSHB_OK(pos < (uint32_t)n && i < (uint32_t)cnt)) {
+                kout[tb + pos] = kr[i];
+                iout[tb + pos] = IMPLICIT_IDS ? id_base + (uint32_t)(tile * kG1Tile) + i : __ldg(ir + i);
+            }
         }
     }
 }
@@ -898,7 +900,7 @@ __global__ void __launch_bounds__(kG2Threads) g2_big(G2Args a) {
         uint32_t heads = 0;
         for (int64_t r = threadIdx.x; r < len; r += kG2Threads) {
             const uint32_t pr = p0[r];
-            od[r] = gi[pr];
+            if (LSHB_OK(pr < (uint32_t)len)) od[r] = gi[pr];
             heads += (r == 0 || gk[p0[r - 1]] != gk[pr]) ? 1u : 0u;
         }
         uint32_t tot;
@@ -1031,7 +1033,7 @@ __device__ void g2a_big_emit(const G2Args& a, int t, int bin, int64_t lo, int le
         const bool h = p < len && (p == 0 || k != gk[perm[p - 1]]);
         uint32_t all;
         const uint32_t ex = cblock_excl_scan(h ? 1u : 0u, ws, &all);
-        if (h) {
+        if (h && LSHB_OK((int64_t)b + ex < n)) {
             uk[b + ex] = k;
             of[b + ex] = (uint32_t)(lo + p);
         }
@@ -1145,6 +1147,7 @@ __device__ __forceinline__ void g2_bin(const G2Args& a, G2aSmem& S, int t, int b
             const uint32_t s1 = d == dmask ? (uint32_t)len
                                            : ((d & 1u) ? (S.cnt[(d + 1) >> 1] & 0xffffu) : (w0 >> 16));
             const uint32_t p = s0 + r;
+            if (!LSHB_OK(p < (uint32_t)len)) continue;
             S.sk[p] = kr[j];
             S.si[p] = ir[j];
             if (s1 - s0 == 1) {
@@ -1204,7 +1207,7 @@ __device__ __forceinline__ void g2_bin(const G2Args& a, G2aSmem& S, int t, int b
 #pragma unroll
     for (int j = 0; j < kG2aIPT; ++j) {
         const int i = u + j * kG2aT;
-        if (i < len && dr[j] != kDone) {
+        if (i < len && dr[j] != kDone && LSHB_OK(dr[j] < (uint32_t)len)) {
             S.sk[dr[j]] = kr[j];
             S.si[dr[j]] = ir[j];
         }
@@ -1225,10 +1228,11 @@ __device__ __forceinline__ void g2_bin(const G2Args& a, G2aSmem& S, int t, int b
     uint32_t* of = a.out.offs + (int64_t)t * (n + 1);
     if (agg == (uint32_t)len) {
         // every key distinct (the common case for fingerprints): bucket p = item p
-        for (int p = u; p < len; p += kG2aT) {
-            __stcs(uk + base + p, S.sk[p]);
-            __stcs(of + base + p, (uint32_t)(lo + p));
-        }
+        if (LSHB_OK((int64_t)base + len <= n))
+            for (int p = u; p < len; p += kG2aT) {
+                __stcs(uk + base + p, S.sk[p]);
+                __stcs(of + base + p, (uint32_t)(lo + p));
+            }
     } else {
         uint32_t b = base;
         for (int p0 = 0; p0 < len; p0 += kG2aT) {
@@ -1237,7 +1241,7 @@ __device__ __forceinline__ void g2_bin(const G2Args& a, G2aSmem& S, int t, int b
             const bool h = p < len && (p == 0 || k != S.sk[p - 1]);
             uint32_t all;
             const uint32_t ex = cblock_excl_scan(h ? 1u : 0u, S.ws, &all);
-            if (h) {
+            if (h && LSHB_OK((int64_t)b + ex < n)) {
                 __stcs(uk + b + ex, k);
                 __stcs(of + b + ex, (uint32_t)(lo + p));
             }
@@ -1310,8 +1314,10 @@ __global__ void __launch_bounds__(kG2Threads) g3_rle(const uint64_t* __restrict_
 #pragma unroll
     for (int j = 0; j < VP; ++j)
         if ((hm >> j) & 1u) {
-            uk[ub] = kv[j];
-            of[ub] = (uint32_t)(r0 + j);
+            if (LSHB_OK(ub < (uint32_t)n)) {
+                uk[ub] = kv[j];
+                of[ub] = (uint32_t)(r0 + j);
+            }
             ++ub;
         }
     if (threadIdx.x == 0 && c == nchunks - 1) {

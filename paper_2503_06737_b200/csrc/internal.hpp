@@ -5,6 +5,17 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Device-side bounds checks of the checked build (build.py --variant checked,
+// -DLSHB_CHECKS): LSHB_OK(cond) guards a write — a failed check prints the site and
+// skips the write (tools/gpu_checked.sh greps for "LSHB_DCHECK").  In the product
+// build it is `true` and vanishes.  (compute-sanitizer is closed on this GPU pool.)
+#ifdef LSHB_CHECKS
+#include <cstdio>
+#define LSHB_OK(c) ((c) ? true : (printf("LSHB_DCHECK %s:%d\n", __FILE__, __LINE__), false))
+#else
+#define LSHB_OK(c) true
+#endif
+
 namespace lshb {
 
 // ---------------------------------------------------------------------------

@@ -159,6 +159,7 @@ __global__ void __launch_bounds__(kQT) knn_kernel(KnnArgs a, int P) {
     const float* q = a.Q + qi * a.ldq;
     for (int j = warp; j < u; j += kQW) {
         const uint32_t id = cand[j];
+        if (!LSHB_OK(id >= a.id_base && (int64_t)(id - a.id_base) < a.n)) continue;   // (checked build only)
         const float* x = a.X + (int64_t)(id - a.id_base) * a.ldx;
         float s0 = 0.f, s1 = 0.f;   // L2: sum (x-q)^2 | cosine: x.q, |x|^2
         if (a.vec) {

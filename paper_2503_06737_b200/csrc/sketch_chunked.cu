@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else if (KT > 0 && KT <= 32) {
                 f = sbits;
             }
-            if (valid && out.keys) out.keys[(int64_t)t * n + row] = E2 ? fk.key() : f;
+            if (valid && out.keys && LSHB_OK(row < n)) out.keys[(int64_t)t * n + row] = E2 ? fk.key() : f;
         }
         if (!has_next) break;
         columns_for_chunk(cn);

@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     else fp |= (uint64_t)zc << kk;
                 }
             }
-            if (valid && out.keys) out.keys[(int64_t)(g * tpb + tb) * n + row] = E2 ? fk.key() : fp;
+            if (valid && out.keys && LSHB_OK(row < n)) out.keys[(int64_t)(g * tpb + tb) * n + row] = E2 ? fk.key() : fp;
         }
         return false;
     };

@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int kk = 0; kk < KT; ++kk) sb |= (acc[kk] > 0.0f ? 1u : 0u) << kk;
                     f = sb;
                 }
-                if (valid && out.keys) out.keys[(int64_t)t * n + row] = f;
+                if (valid && out.keys && LSHB_OK(row < n)) out.keys[(int64_t)t * n + row] = f;
             }
         } else {
             // generic K (and the debug outputs): sequential sum over each bin's coordinates
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (!E2 && out.bits && z) atomicOr(&out.bits[row * ((m + 31) >> 5) + (l >> 5)], 1u << (l & 31));
                     }
                 }
-                if (valid && out.keys) out.keys[(int64_t)t * n + row] = E2 ? fk.key() : sbits;
+                if (valid && out.keys && LSHB_OK(row < n)) out.keys[(int64_t)t * n + row] = E2 ? fk.key() : sbits;
             }
         }
         if (!has_next) break;
