@@ -156,11 +156,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     float4 buf[VEC ? RG * 4 : VS];
 
-    auto load = [&](int64_t tl) {
+    // row groups [i0, i1) of the thread's column (VEC); the scalar path ignores them
+    auto load = [&](int64_t tl, int i0 = 0, int i1 = 1 << 20) {
         if constexpr (VEC) {
             if (col_ok) {
 #pragma unroll
                 for (int i = 0; i < RG; ++i) {
+                    if (i < i0 || i >= i1) continue;
                     const int64_t r = tl * 32 + 4 * (rg + NG * i);
                     const float* src = X + r * ld + 4 * c;
                     if (tl * 32 + 32 <= n) {
@@ -188,11 +190,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     };
-    auto store = [&]() {
+    auto store = [&](int i0 = 0, int i1 = 1 << 20) {
         if constexpr (VEC) {
             if (col_ok) {
 #pragma unroll
                 for (int i = 0; i < RG; ++i) {
+                    if (i < i0 || i >= i1) continue;
                     float* dst = T + c * CW + 4 * (rg + NG * i);
                     const float4 a = buf[4 * i], b = buf[4 * i + 1], cc = buf[4 * i + 2], e = buf[4 * i + 3];
                     sts128(dst, __float_as_uint(a.x) ^ sm[0], __float_as_uint(b.x) ^ sm[0],
@@ -228,11 +231,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float* Tl = Tw;
     while (true) {
         __syncthreads();  // previous gathers finished with T
-        store();
-        __syncthreads();
         const int64_t ntile = tile + gridDim.x;
         const bool has_next = ntile < ntiles;
-        if (has_next) load(ntile);  // in flight during the gathers below
+        // the next tile's loads go out as soon as their registers are stored (in halves),
+        // so HBM stays busy through the staging phase and the barrier
+        if constexpr (VEC && RG >= 2) {
+            store(0, RG / 2);
+            if (has_next) load(ntile, 0, RG / 2);
+            store(RG / 2, RG);
+            if (has_next) load(ntile, RG / 2, RG);
+        } else {
+            store();
+            if (has_next) load(ntile);
+        }
+        __syncthreads();   // the loads above are in flight during the gathers below
         const int64_t row = tile * 32 + lane;
         const bool valid = row < n;
         if constexpr (KT > 0) {
