@@ -21,7 +21,7 @@ from bench import source_hash  # noqa: E402
 TIMING = [("sketch_kernel", "sketch"), ("sketch_chunked", "sketch"), ("sketch_hcs", "sketch"),
           ("g0_mask", "group_hist"), ("g0_spec", "group_hist"), ("g1_hist", "group_hist"),
           ("g1_scan", "group_scan"), ("g1_binstart", "group_scan"), ("g1_scatter", "group_scatter"),
-          ("g2_big", "group_sort"), ("g2w", "group_sort"), ("g3_rle", "group_sort"), ("lookup", "lookup"),
+          ("g2_big", "group_sort"), ("g2a", "group_sort"), ("g3_rle", "group_sort"), ("lookup", "lookup"),
           ("dense_tc", "dense_gemm"), ("split3", "dense_gemm")]
 WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
