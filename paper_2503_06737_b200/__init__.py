@@ -15,8 +15,8 @@ from typing import Optional, Sequence, Tuple
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liblsh_b200.so")
-if os.environ.get("LSH_LIB_VARIANT") == "checked":   # device bounds-checked build (tools/gpu_checked.sh)
-    LIB_PATH = os.path.join(_HERE, "liblsh_b200_checked.so")
+if os.environ.get("LSH_LIB_VARIANT"):   # e.g. "checked": device bounds-checked build (tools/gpu_checked.sh)
+    LIB_PATH = os.path.join(_HERE, f"liblsh_b200_{os.environ['LSH_LIB_VARIANT']}.so")
 
 SCHEMES = {"E2LSH": 0, "SRP": 1, "CS_E2LSH": 2, "CS_SRP": 3, "HCS_E2LSH": 4, "HCS_SRP": 5}
 STATUS = {0: "LSH_OK", 1: "LSH_EINVAL", 2: "LSH_EDIM", 3: "LSH_ENOMEM", 4: "LSH_ECUDA", 5: "LSH_EOVERFLOW",

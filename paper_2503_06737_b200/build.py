@@ -17,6 +17,10 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "liblsh_b200.so")
 SOURCES = ["api.cu", "sketch.cu", "sketch_fast.cu", "sketch_chunked.cu", "sketch_hcs.cu", "group.cu", "dense_tc.cu", "knn.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# measurement-only variants (liblsh_b200_<name>.so, loaded with LSH_LIB_VARIANT=<name>)
+# (C4, measured round 2: 2048 L1 bins of ~488 keys with IPT 5 / D 11 — scatter 0.44 ->
+#  0.56 ms, per-bin sort unchanged at 0.87 ms — not kept)
+VARIANT_FLAGS = {"b11": ["-DLSHB_G2_IPT=5", "-DLSHB_G2_D=11", "-DLSHB_L1_AVG=512"]}
 
 
 def nvcc() -> str:
@@ -52,6 +56,7 @@ def build(verbose: bool = False, force: bool = False, variant: str = "") -> str:
         flags += ["-Xptxas", "-v"]
     if variant == "checked":
         flags += ["-DLSHB_CHECKS"]
+    flags += VARIANT_FLAGS.get(variant, [])
     procs = []
     for src in SOURCES:
         obj = os.path.join(tmp, src.replace(".cu", ".o"))

@@ -37,7 +37,16 @@ constexpr int kG1Threads = 256;
 constexpr int kG2Threads = 512;
 constexpr int kG2Warps = kG2Threads / 32;       // 16
 constexpr int kG2Cap = 4096;                    // run-length-encoding chunk (narrow keys)
-constexpr int kG2BinCap = 1280;                 // largest L1 bin sorted in shared memory (g2a)
+#ifndef LSHB_G2_IPT
+#define LSHB_G2_IPT 10   // items per thread of the per-bin sort (g2a): cap 128 * IPT
+#endif
+#ifndef LSHB_G2_D
+#define LSHB_G2_D 12     // counting-sort digit bits inside a bin
+#endif
+#ifndef LSHB_L1_AVG
+#define LSHB_L1_AVG 1024 // L1 bins hold at most this many keys on average
+#endif
+constexpr int kG2BinCap = 128 * LSHB_G2_IPT;    // largest L1 bin sorted in shared memory (g2a)
 
 size_t group_tiles(int64_t n) { return (size_t)((n + kG1Tile - 1) / kG1Tile); }
 
@@ -49,7 +58,7 @@ bool group_is_lsd(int W) { return W <= 22; }
 int group_l1_bits(int64_t n, int W) {
     if (group_is_lsd(W)) return (W + 1) / 2;
     int b = 1;
-    while (b < 11 && ((n + (1ll << b) - 1) >> b) > 1024) ++b;   // bins of <= 1024 on average (cap 1280)
+    while (b < 11 && ((n + (1ll << b) - 1) >> b) > LSHB_L1_AVG) ++b;   // bins of <= LSHB_L1_AVG on average
     return b < W ? b : W;
 }
 
@@ -927,9 +936,9 @@ __global__ void __launch_bounds__(kG2Threads) g2_big(G2Args a) {
 // ---------------------------------------------------------------------------
 constexpr int kG2aT = 128;
 constexpr int kG2aW = kG2aT / 32;
-constexpr int kG2aIPT = 10;
+constexpr int kG2aIPT = LSHB_G2_IPT;
 constexpr int kG2aCap = kG2aT * kG2aIPT;      // 1280 items
-constexpr int kG2aD = 12;                      // digit bits (4096 counters)
+constexpr int kG2aD = LSHB_G2_D;               // digit bits (2^D counters)
 constexpr int kG2aCW = 1 << (kG2aD - 1);       // counter words (two u16 counters each)
 constexpr int kG2aLong = 64;                   // longest segment ranked item by item
 constexpr int kG2aLongMax = kG2aCap / kG2aLong;

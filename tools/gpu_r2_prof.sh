@@ -3,7 +3,7 @@
 mkdir -p gpurun_out/r2/prof2
 P=gpurun_out/r2/prof2
 K=${KERNELS:-"sketch_kernel|g1_hist|g1_scatter|g2a"}
-ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "profile/" -k regex:"$K" -o /tmp/p2 \
+ncu -f --set full --clock-control none --import-source on --nvtx --nvtx-include "profile/" -k regex:"$K" -o /tmp/p2 \
     python tools/prof_hash.py --config ${CFG:-C4} --scheme ${SCHEME:-CS_E2LSH} --op build --reps 1 > $P/ncu.log 2>&1
 ncu -i /tmp/p2.ncu-rep --page raw --csv > $P/raw.csv 2>/dev/null
 for k in $(echo $K | tr '|' ' '); do
