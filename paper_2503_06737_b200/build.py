@@ -20,7 +20,10 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # measurement-only variants (liblsh_b200_<name>.so, loaded with LSH_LIB_VARIANT=<name>)
 # (C4, measured round 2: 2048 L1 bins of ~488 keys with IPT 5 / D 11 — scatter 0.44 ->
 #  0.56 ms, per-bin sort unchanged at 0.87 ms — not kept)
-VARIANT_FLAGS = {"b11": ["-DLSHB_G2_IPT=5", "-DLSHB_G2_D=11", "-DLSHB_L1_AVG=512"]}
+VARIANT_FLAGS = {"b11": ["-DLSHB_G2_IPT=5", "-DLSHB_G2_D=11", "-DLSHB_L1_AVG=512"],
+                 # (C4: 4096-key tiles, 2 scatter CTAs per SM — E2LSH scatter 0.44 -> 0.92 ms
+                 #  (shorter runs, more partial sectors), SRP 1.34 -> 1.22 ms — not kept)
+                 "t4k": ["-DLSHB_G1_TILE=4096", "-DLSHB_SCATTER_CPS=2"]}
 
 
 def nvcc() -> str:

@@ -32,7 +32,13 @@
 
 namespace lshb {
 
-constexpr int kG1Tile = 8192;                   // items per L1 tile
+#ifndef LSHB_G1_TILE
+#define LSHB_G1_TILE 8192
+#endif
+#ifndef LSHB_SCATTER_CPS
+#define LSHB_SCATTER_CPS 1   // L1 scatter CTAs per SM
+#endif
+constexpr int kG1Tile = LSHB_G1_TILE;           // items per L1 tile
 constexpr int kG1Threads = 256;
 constexpr int kG2Threads = 512;
 constexpr int kG2Warps = kG2Threads / 32;       // 16
@@ -364,7 +370,7 @@ size_t g1_scatter_smem(int nb1, bool stable, int nst) {
 // per-chunk sort orders ties by id).  STABLE = true (narrow-key LSD passes, which
 // need stability): warp-private counts + ballot digit match.
 template <bool IMPLICIT_IDS, bool STABLE>
-__global__ void __launch_bounds__(kSThreads, 1)
+__global__ void __launch_bounds__(kSThreads, LSHB_SCATTER_CPS)
     g1_scatter(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ iin, uint64_t* __restrict__ kout,
                uint32_t* __restrict__ iout, int64_t n, const L1Spec* __restrict__ spec, int nb1,
                const uint32_t* __restrict__ hist, const uint32_t* __restrict__ binstart, int T, int L,
@@ -1372,7 +1378,7 @@ static cudaError_t l1_pass(const uint64_t* kin, const uint32_t* iin, uint64_t* k
     int nst = 2;
     const size_t sm1 = g1_scatter_smem(nb1, stable || ids, nst);
     const int64_t items = (int64_t)T * L;
-    const int grid = (int)std::min<int64_t>(items, (int64_t)num_sms);
+    const int grid = (int)std::min<int64_t>(items, (int64_t)num_sms * LSHB_SCATTER_CPS);
     cudaError_t e;
     if (!ids) {
         if (stable) {
