@@ -687,8 +687,9 @@ extern "C" lsh_status lsh_create(const lsh_params* p, lsh_handle** out) {
     if ((e = cudaMalloc(&H->d_coff, sizeof(float) * m)) != cudaSuccess) return fail(cuda_fail(e, "malloc"));
     if ((e = cudaMemcpy(H->d_coff, coff.data(), sizeof(float) * m, cudaMemcpyHostToDevice)) != cudaSuccess)
         return fail(cuda_fail(e, "memcpy"));
-    if ((e = cudaMalloc(&H->d_flags, sizeof(int))) != cudaSuccess) return fail(cuda_fail(e, "malloc"));
-    if ((e = cudaMemset(H->d_flags, 0, sizeof(int))) != cudaSuccess) return fail(cuda_fail(e, "memset"));
+    // [0] sticky device status (overflow), [1] grouping-path hint (group.cu: launch_group)
+    if ((e = cudaMalloc(&H->d_flags, 2 * sizeof(int))) != cudaSuccess) return fail(cuda_fail(e, "malloc"));
+    if ((e = cudaMemset(H->d_flags, 0, 2 * sizeof(int))) != cudaSuccess) return fail(cuda_fail(e, "memset"));
     H->disc.c_off = H->d_coff;
     H->disc.flags = H->d_flags;
     if ((e = cudaMalloc(&H->d_b, sizeof(float) * m)) != cudaSuccess) return fail(cuda_fail(e, "malloc"));
@@ -860,8 +861,10 @@ static lsh_status group_impl(const lsh_handle* H, const uint64_t* keys, uint64_t
     const int L = H->p.L;
     GroupScratch sc{};
     const size_t nb1 = (size_t)group_bins(n, H->key_width);
-    const size_t b_keys = sizeof(uint64_t) * (size_t)L * n;
-    const size_t b_ids = sizeof(uint32_t) * (size_t)L * n;
+    // L1 output: [L][n] (histogram path) or the fixed-capacity layout [L][nb1][cap]
+    const size_t slots = group_key_slots(n, H->key_width);
+    const size_t b_keys = sizeof(uint64_t) * (size_t)L * slots;
+    const size_t b_ids = sizeof(uint32_t) * (size_t)L * slots;
     const size_t b_hist = sizeof(uint32_t) * (size_t)L * std::max<size_t>(group_hist_words(n, H->key_width), 1);
     const size_t b_tot = sizeof(uint32_t) * (size_t)L * nb1;
     const size_t b_bs = sizeof(uint32_t) * (size_t)L * (nb1 + 1);
@@ -870,7 +873,7 @@ static lsh_status group_impl(const lsh_handle* H, const uint64_t* keys, uint64_t
     const size_t b_perm = own_perm ? b_keys : 0;
     const size_t b_vm = sizeof(unsigned long long) * 2 * (size_t)L;
     const size_t b_spec = group_spec_bytes() * 2 * (size_t)L;
-    const size_t b_cb = sizeof(uint32_t) * ((size_t)L * nb1 + 2);   // big-bin count, g2a ticket, big-bin list
+    const size_t b_cb = sizeof(uint32_t) * ((size_t)L * nb1 + 3);   // big-bin count, g2a ticket, overflow, big-bin list
     void* mem = nullptr;
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
     const size_t total = al(b_keys) + al(b_ids) + al(b_hist) + al(b_tot) + al(b_bs) + al(b_st) + al(b_perm) + al(b_vm) +
@@ -893,7 +896,7 @@ static lsh_status group_impl(const lsh_handle* H, const uint64_t* keys, uint64_t
         sc.vmask = (unsigned long long*)take(b_vm);
         sc.spec = take(b_spec);
         sc.bigcount = (uint32_t*)take(b_cb);
-        sc.biglist = sc.bigcount + 2;
+        sc.biglist = sc.bigcount + 3;
     }
     sc.num_sms = H->num_sms;
     cudaError_t e = launch_group(keys, n, L, (uint32_t)id_base, H->key_width, sc, I->dev, H->d_flags, s);

@@ -186,7 +186,8 @@ __device__ L1Spec make_spec(const int* pos, int nb) {
 // passes == 1 (MSD): the top B1 varying bits.  passes == 2 (LSD, narrow keys): the
 // varying bits split into a low half (pass 0) and a high half (pass 1), each <= B1.
 __global__ void g0_spec(const unsigned long long* __restrict__ vm, int L, int B1, int passes,
-                        L1Spec* __restrict__ spec) {
+                        L1Spec* __restrict__ spec, const uint32_t* __restrict__ gate = nullptr) {
+    if (gate && *gate == 0u) return;   // (gated: runs only as the fixed-capacity path's fallback)
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= L) return;
     const uint64_t V = vm[2 * t] & vm[2 * t + 1];
@@ -212,67 +213,76 @@ __global__ void g0_spec(const unsigned long long* __restrict__ vm, int L, int B1
 // accumulated for the varying-bit mask in the same read.  mode 2: redo mode 1's
 // histogram with the spec digit, only for tables whose varying top bits are not the
 // top b1 bits (other CTAs exit at once).
+// Grid-stride over the (table, tile) items (item = t * T + tile) so that a gated launch
+// (the fixed-capacity path's fallback) is a few hundred CTAs that exit at once.
 __global__ void __launch_bounds__(kG1Threads) g1_hist(const uint64_t* __restrict__ keys, int64_t n,
                                                     const L1Spec* __restrict__ spec, int nb1,
                                                     uint32_t* __restrict__ hist, int T, int mode, int W, int b1,
-                                                    unsigned long long* __restrict__ vm) {
+                                                    unsigned long long* __restrict__ vm,
+                                                    const uint32_t* __restrict__ gate = nullptr, int L = 0) {
     extern __shared__ uint32_t g1_cnt[];
-    const int t = blockIdx.y, tile = blockIdx.x;
-    L1Spec sp;
-    if (mode == 1) {
-        sp.nbits = b1;
-        sp.shift = W - b1;
-        sp.below = 0;
-    } else {
-        sp = spec[t];
-        if (mode == 2 && sp.nbits == b1 && sp.shift == W - b1) return;
-    }
-    uint64_t o = 0, no = 0;
-    for (int i = threadIdx.x; i < nb1; i += kG1Threads) g1_cnt[i] = 0;
-    const int64_t t0 = (int64_t)tile * kG1Tile;
-    const uint64_t* kt = keys + (int64_t)t * n + t0;
-    const int cn = (int)min((int64_t)kG1Tile, n - t0);
-    constexpr int R = 16;   // keys per thread per batch
-#pragma unroll 1
-    for (int b0 = 0; b0 < kG1Tile; b0 += R * kG1Threads) {
-        uint64_t k[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int i = b0 + r * kG1Threads + threadIdx.x;
-            k[r] = i < cn ? __ldcs(kt + i) : 0ull;
+    if (gate && *gate == 0u) return;
+    for (int64_t item = blockIdx.x; item < (int64_t)T * L; item += gridDim.x) {
+        const int t = (int)(item / T), tile = (int)(item % T);
+        L1Spec sp;
+        if (mode == 1) {
+            sp.nbits = b1;
+            sp.shift = W - b1;
+            sp.below = 0;
+        } else {
+            sp = spec[t];
+            if (mode == 2 && sp.nbits == b1 && sp.shift == W - b1) continue;
         }
-        if (b0 == 0) __syncthreads();   // counters cleared
+        uint64_t o = 0, no = 0;
+        __syncthreads();   // the previous item's counters are written out
+        for (int i = threadIdx.x; i < nb1; i += kG1Threads) g1_cnt[i] = 0;
+        const int64_t t0 = (int64_t)tile * kG1Tile;
+        const uint64_t* kt = keys + (int64_t)t * n + t0;
+        const int cn = (int)min((int64_t)kG1Tile, n - t0);
+        constexpr int R = 16;   // keys per thread per batch
+#pragma unroll 1
+        for (int b0 = 0; b0 < kG1Tile; b0 += R * kG1Threads) {
+            uint64_t k[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int i = b0 + r * kG1Threads + threadIdx.x;
-            if (i < cn) {
-                atomicAdd(&g1_cnt[l1_digit(k[r], sp)], 1u);
-                if (mode == 1) {
-                    o |= k[r];
-                    no |= ~k[r];
+            for (int r = 0; r < R; ++r) {
+                const int i = b0 + r * kG1Threads + threadIdx.x;
+                k[r] = i < cn ? __ldcs(kt + i) : 0ull;
+            }
+            if (b0 == 0) __syncthreads();   // counters cleared
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int i = b0 + r * kG1Threads + threadIdx.x;
+                if (i < cn) {
+                    atomicAdd(&g1_cnt[l1_digit(k[r], sp)], 1u);
+                    if (mode == 1) {
+                        o |= k[r];
+                        no |= ~k[r];
+                    }
                 }
             }
         }
-    }
-    if (mode == 1) {
+        if (mode == 1) {
 #pragma unroll
-        for (int sft = 16; sft > 0; sft >>= 1) {
-            o |= __shfl_xor_sync(0xffffffffu, o, sft);
-            no |= __shfl_xor_sync(0xffffffffu, no, sft);
+            for (int sft = 16; sft > 0; sft >>= 1) {
+                o |= __shfl_xor_sync(0xffffffffu, o, sft);
+                no |= __shfl_xor_sync(0xffffffffu, no, sft);
+            }
+            if ((threadIdx.x & 31) == 0) {
+                atomicOr(vm + 2 * t, (unsigned long long)o);
+                atomicOr(vm + 2 * t + 1, (unsigned long long)no);
+            }
         }
-        if ((threadIdx.x & 31) == 0) {
-            atomicOr(vm + 2 * t, (unsigned long long)o);
-            atomicOr(vm + 2 * t + 1, (unsigned long long)no);
-        }
+        __syncthreads();
+        uint32_t* row = hist + ((int64_t)t * T + tile) * nb1;
+        for (int b = threadIdx.x; b < nb1; b += kG1Threads) row[b] = g1_cnt[b];
     }
-    __syncthreads();
-    uint32_t* row = hist + ((int64_t)t * T + tile) * nb1;
-    for (int b = threadIdx.x; b < nb1; b += kG1Threads) row[b] = g1_cnt[b];
 }
 
 // One warp per (table, 32 consecutive bins), lane = bin: exclusive running sum over
 // the tiles in place (coalesced rows of the tile-major counts), bin totals out.
-__global__ void g1_scan(uint32_t* __restrict__ hist, int T, int L, int nb1, uint32_t* __restrict__ tot) {
+__global__ void g1_scan(uint32_t* __restrict__ hist, int T, int L, int nb1, uint32_t* __restrict__ tot,
+                        const uint32_t* __restrict__ gate = nullptr) {
+    if (gate && *gate == 0u) return;
     const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int groups = (nb1 + 31) / 32;
@@ -303,8 +313,10 @@ __global__ void g1_scan(uint32_t* __restrict__ hist, int T, int L, int nb1, uint
 // list (wide keys), every bin larger than kG2BinCap is appended as t * nb1 + bin.
 __global__ void __launch_bounds__(1024) g1_binstart(const uint32_t* __restrict__ tot, int nb1, int64_t n,
                                                     uint32_t* __restrict__ binstart, uint32_t* __restrict__ biglist,
-                                                    uint32_t* __restrict__ bigcount) {
+                                                    uint32_t* __restrict__ bigcount,
+                                                    const uint32_t* __restrict__ gate = nullptr) {
     __shared__ uint32_t ws[32];
+    if (gate && *gate == 0u) return;
     const int t = blockIdx.x;
     const int b0 = 2 * threadIdx.x, b1 = b0 + 1;
     const uint32_t v0 = b0 < nb1 ? tot[(int64_t)t * nb1 + b0] : 0u;
@@ -317,6 +329,35 @@ __global__ void __launch_bounds__(1024) g1_binstart(const uint32_t* __restrict__
     if (!biglist) return;
     if (b0 < nb1 && v0 > (uint32_t)kG2BinCap) biglist[atomicAdd(bigcount, 1u)] = (uint32_t)t * nb1 + b0;
     if (b1 < nb1 && v1 > (uint32_t)kG2BinCap) biglist[atomicAdd(bigcount, 1u)] = (uint32_t)t * nb1 + b1;
+}
+
+// Fixed-capacity path (wide keys): bin starts from the bins' final cursors (= their
+// sizes) and the digit spec (the top b1 key bits), unless a bin overflowed.
+__global__ void __launch_bounds__(1024) g1_fixscan(const uint32_t* __restrict__ cur, int nb1, int64_t n,
+                                                   uint32_t* __restrict__ binstart, L1Spec* __restrict__ spec,
+                                                   int b1, int W, const uint32_t* __restrict__ ovf,
+                                                   uint32_t* __restrict__ hint) {
+    __shared__ uint32_t ws[32];
+    const uint32_t o = *ovf;
+    if (hint && blockIdx.x == 0 && threadIdx.x == 0) {
+        const uint32_t h = *hint;
+        *hint = (o & 1u) ? 8u : (h > 0u ? h - 1u : 0u);   // real overflow: 8 builds on the histogram path
+    }
+    if (o) return;
+    const int t = blockIdx.x;
+    const int b0 = 2 * threadIdx.x, b1i = b0 + 1;
+    const uint32_t v0 = b0 < nb1 ? cur[(int64_t)t * nb1 + b0] : 0u;
+    const uint32_t v1 = b1i < nb1 ? cur[(int64_t)t * nb1 + b1i] : 0u;
+    const uint32_t e = block_excl_scan<1024>(v0 + v1, ws, nullptr);
+    uint32_t* bs = binstart + (int64_t)t * (nb1 + 1);
+    if (b0 < nb1) bs[b0] = e;
+    if (b1i < nb1) bs[b1i] = e + v0;
+    if (threadIdx.x == 0) {
+        bs[nb1] = (uint32_t)n;
+        int pos[12];
+        for (int j = 0; j < b1; ++j) pos[j] = W - 1 - j;
+        spec[t] = make_spec(pos, b1);
+    }
 }
 
 // Stable scatter by the L1 digit, persistent: CTA c takes work items c, c + grid, ...
@@ -369,13 +410,25 @@ size_t g1_scatter_smem(int nb1, bool stable, int nst) {
 // atomicAdd per key (order inside a tile's run of a digit is then arbitrary; the
 // per-chunk sort orders ties by id).  STABLE = true (narrow-key LSD passes, which
 // need stability): warp-private counts + ballot digit match.
-template <bool IMPLICIT_IDS, bool STABLE>
+// FIX (wide keys, no histogram pass): the digit is the top b1 key bits and every L1 bin
+// has a fixed capacity kG2BinCap in the output ([L][nb1][cap] layout, table stride
+// ostride); a tile reserves its run of each digit with one atomicAdd on the bin's
+// cursor (cursor[t][d] in `hist`).  A bin that would exceed its capacity sets
+// *ovf and its runs are dropped: the histogram path then redoes the grouping.
+// (Fingerprint keys are uniform: a C4 bin holds 977 +- 31 keys, cap 1280.)
+template <bool IMPLICIT_IDS, bool STABLE, bool FIX = false>
 __global__ void __launch_bounds__(kSThreads, LSHB_SCATTER_CPS)
     g1_scatter(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ iin, uint64_t* __restrict__ kout,
                uint32_t* __restrict__ iout, int64_t n, const L1Spec* __restrict__ spec, int nb1,
                const uint32_t* __restrict__ hist, const uint32_t* __restrict__ binstart, int T, int L,
-               uint32_t id_base, int nst) {
+               uint32_t id_base, int nst, const uint32_t* __restrict__ gate = nullptr, uint32_t* __restrict__ ovf = nullptr,
+               int fix_b1 = 0, int fix_w = 64, int64_t ostride = 0, const uint32_t* __restrict__ gate_skip = nullptr) {
     extern __shared__ __align__(128) unsigned char g1_dsm[];
+    if (gate && *gate == 0u) return;
+    if (FIX && gate_skip && *gate_skip) {   // hinted: leave it to the histogram path
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(ovf, 2u);
+        return;
+    }
     uint64_t* bars = reinterpret_cast<uint64_t*>(g1_dsm);                                  // [nst]
     uint64_t* rk = reinterpret_cast<uint64_t*>(g1_dsm + 64);                               // [nst][4096]
     uint16_t* sp = reinterpret_cast<uint16_t*>(rk + (size_t)nst * kG1Tile);                // staged item
@@ -433,11 +486,19 @@ __global__ void __launch_bounds__(kSThreads, LSHB_SCATTER_CPS)
     for (;; advance(cc)) {
         if (cc.t >= L) break;
         const int t = cc.t, tile = cc.tile;
-        const L1Spec sp0 = spec[t];
-        const int64_t tb = (int64_t)t * n;
+        L1Spec sp0;
+        if constexpr (FIX) {
+            sp0.nbits = fix_b1;
+            sp0.shift = fix_w - fix_b1;
+            sp0.below = 0;
+        } else {
+            sp0 = spec[t];
+        }
+        const int64_t tb = (int64_t)t * (FIX ? ostride : n);   // output table base
+        const int64_t ti = (int64_t)t * n;                      // input table base
         const int cnt = (int)min((int64_t)kG1Tile, n - (int64_t)tile * kG1Tile);
         uint64_t* kr = rk + (size_t)st * kG1Tile;
-        const uint32_t* ir = IMPLICIT_IDS ? nullptr : iin + tb + (int64_t)tile * kG1Tile;
+        const uint32_t* ir = IMPLICIT_IDS ? nullptr : iin + ti + (int64_t)tile * kG1Tile;
         // this tile's global run starts per digit.  Stable (LSD) passes: loads issued now,
         // consumed after the ranking (measured: SRP scatter 1.39 -> 1.34 ms); the wide-key
         // pass loads them after the scan (prefetching there measured slower, 0.45 -> 0.55 ms)
@@ -453,7 +514,7 @@ __global__ void __launch_bounds__(kSThreads, LSHB_SCATTER_CPS)
         g_mbar_wait(bars + st, phase);
         for (int i = threadIdx.x; i < (STABLE ? kSWarps * nb1 : 2 * nb1); i += kSThreads) wrun[i] = 0;
         if (!bulk_ok(t, tile)) {
-            for (int i = threadIdx.x; i < cnt; i += kSThreads) kr[i] = kin[tb + (int64_t)tile * kG1Tile + i];
+            for (int i = threadIdx.x; i < cnt; i += kSThreads) kr[i] = kin[ti + (int64_t)tile * kG1Tile + i];
         }
         __syncthreads();   // tile in smem; previous write-out finished with its stage
         if (threadIdx.x == 0) {
@@ -528,7 +589,18 @@ __global__ void __launch_bounds__(kSThreads, LSHB_SCATTER_CPS)
                 const uint32_t c = loc[d];
                 loc[d] = ex;
                 ex += c;
-                gpos[d] = STABLE ? gp[j] : binstart[(int64_t)t * (nb1 + 1) + d] + hist[((int64_t)t * T + tile) * nb1 + d];
+                if constexpr (FIX) {
+                    uint32_t g = 0xffffffffu;
+                    if (c) {
+                        const uint32_t b0 = atomicAdd(const_cast<uint32_t*>(hist) + (int64_t)t * nb1 + d, c);
+                        if (b0 + c <= (uint32_t)kG2BinCap) g = (uint32_t)d * kG2BinCap + b0;
+                        else atomicOr(ovf, 1u);
+                    }
+                    gpos[d] = g;
+                } else {
+                    gpos[d] = STABLE ? gp[j]
+                                     : binstart[(int64_t)t * (nb1 + 1) + d] + hist[((int64_t)t * T + tile) * nb1 + d];
+                }
             }
         }
         __syncthreads();
@@ -545,8 +617,9 @@ __global__ void __launch_bounds__(kSThreads, LSHB_SCATTER_CPS)
         __syncthreads();
         for (int p = threadIdx.x; p < cnt; p += kSThreads) {
             const uint32_t i = sp[p], dg = sd[p];
+            if (FIX && gpos[dg] == 0xffffffffu) continue;   // overflowed bin: the fallback redoes it
             const uint32_t pos = gpos[dg] + ((uint32_t)p - loc[dg]);
-            if (LSHB_OK(pos < (uint32_t)n && i < (uint32_t)cnt)) {
+            if (LSHB_OK(pos < (uint32_t)(FIX ? ostride : n) && i < (uint32_t)cnt)) {
                 kout[tb + pos] = kr[i];
                 iout[tb + pos] = IMPLICIT_IDS ? id_base + (uint32_t)(tile * kG1Tile) + i : __ldg(ir + i);
             }
@@ -572,6 +645,8 @@ struct G2Args {
     const uint32_t* bigcount;   // [1] entries of biglist
     uint32_t* binheads;         // [L][nb1] buckets per bin (big bins: written by g2_big)
     uint32_t* ticket;           // [1] g2a's dynamic bin counter (zero before the launch)
+    const uint32_t* ovf;        // fixed-capacity L1 layout unless *ovf (nullptr: compact layout)
+    int64_t fix_tstride;        // fixed layout: table stride of keys / ids (nb1 * kG2BinCap)
     IndexDev out;
 };
 
@@ -1290,7 +1365,10 @@ __global__ void __launch_bounds__(kG2aT, 6) g2a(G2Args a) {
         g2a_big_emit(a, t, bin, lo, len, &s_base);
         return;
     }
-    g2_bin(a, S, t, bin, lo, len, a.keys + (int64_t)t * n + lo, a.ids + (int64_t)t * n + lo, nullptr, &s_base);
+    // source of the bin's items: the fixed-capacity L1 layout [t][bin][cap], or compact
+    const int64_t src = (a.ovf && *a.ovf == 0u) ? (int64_t)t * a.fix_tstride + (int64_t)bin * kG2aCap
+                                                : (int64_t)t * n + lo;
+    g2_bin(a, S, t, bin, lo, len, a.keys + src, a.ids + src, nullptr, &s_base);
 }
 
 // Run-length encoding of fully sorted keys (LSD path): chunk c = items
@@ -1350,7 +1428,15 @@ size_t group_hist_words(int64_t n, int W) {
 }
 int group_bins(int64_t n, int W) { return 1 << group_l1_bits(n, W); }
 int group_rle_chunks(int64_t n) { return (int)((n + kG2Cap - 1) / kG2Cap); }
+size_t group_key_slots(int64_t n, int W) {
+    if (n == 0 || group_is_lsd(W)) return (size_t)n;
+    return std::max<size_t>((size_t)n, (size_t)group_bins(n, W) * kG2BinCap);
+}
 size_t group_spec_bytes() { return sizeof(L1Spec); }
+
+static unsigned hist_grid(int T, int L, int num_sms) {
+    return (unsigned)std::min<int64_t>((int64_t)T * L, (int64_t)num_sms * 8);
+}
 
 // One L1 counting pass (histogram, tile scan, bin starts, stable scatter) of every
 // table by the digit of spec[0..L).
@@ -1359,10 +1445,10 @@ static cudaError_t l1_pass(const uint64_t* kin, const uint32_t* iin, uint64_t* k
                            uint32_t* bigcount, int num_sms, cudaStream_t s, bool hist_done = false,
                            bool stable = true) {
     const int T = (int)group_tiles(n);
-    const dim3 g1(T, L);
     if (!hist_done) {
         timing_begin("group_hist", s);
-        g1_hist<<<g1, kG1Threads, nb1 * sizeof(uint32_t), s>>>(kin, n, spec, nb1, sc.hist, T, 0, 64, 0, nullptr);
+        g1_hist<<<hist_grid(T, L, num_sms), kG1Threads, nb1 * sizeof(uint32_t), s>>>(kin, n, const_cast<L1Spec*>(spec), nb1,
+                                                                               sc.hist, T, 0, 64, 0, nullptr, nullptr, L);
         count_launch();
         timing_end("group_hist", s);
     }
@@ -1405,7 +1491,11 @@ static cudaError_t l1_pass(const uint64_t* kin, const uint32_t* iin, uint64_t* k
 
 cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_base, int W, GroupScratch& sc,
                          IndexDev& out, int* flags, cudaStream_t s) {
-    (void)flags;
+    // flags[1]: the handle's grouping-path hint (wide keys): > 0 after a build whose
+    // fixed-capacity L1 pass overflowed (duplicate-heavy codes): the next builds go
+    // straight to the histogram path, retrying the fixed one after 8 builds.  Only
+    // the speed depends on it: both paths produce the same canonical index.
+    uint32_t* hint = flags ? reinterpret_cast<uint32_t*>(flags + 1) : nullptr;
     cudaError_t e;
     if (n == 0) {
         e = cudaMemsetAsync(out.nb, 0, sizeof(uint32_t) * L, s);
@@ -1420,18 +1510,7 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
     e = cudaMemsetAsync(sc.vmask, 0, sizeof(unsigned long long) * 2 * L, s);
     if (e != cudaSuccess) return e;
     const int T = (int)group_tiles(n);
-    if (!lsd) {
-        // wide keys: one read of the keys gives the top-B1-bit histograms AND the
-        // varying mask; tables whose top B1 bits do not all vary are re-histogrammed
-        g1_hist<<<dim3(T, L), kG1Threads, nb1 * sizeof(uint32_t), s>>>(keys, n, spec, nb1, sc.hist, T, 1, W, B1,
-                                                                      sc.vmask);
-        count_launch();
-        g0_spec<<<(L + 127) / 128, 128, 0, s>>>(sc.vmask, L, B1, 1, spec);
-        count_launch();
-        g1_hist<<<dim3(T, L), kG1Threads, nb1 * sizeof(uint32_t), s>>>(keys, n, spec, nb1, sc.hist, T, 2, W, B1,
-                                                                      nullptr);
-        count_launch();
-    } else {
+    if (lsd) {
         g0_mask<<<dim3((unsigned)((n + 8191) / 8192), L), 256, 0, s>>>(keys, n, sc.vmask);
         count_launch();
         g0_spec<<<(L + 127) / 128, 128, 0, s>>>(sc.vmask, L, B1, 2, spec);
@@ -1454,13 +1533,66 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
         timing_end("group_sort", s);
         return cudaGetLastError();
     }
-    e = cudaMemsetAsync(sc.bigcount, 0, 2 * sizeof(uint32_t), s);   // big-bin count, g2a ticket
+    // wide keys.  (1) fixed-capacity L1 scatter on the top B1 bits with per-bin cursors
+    // (no histogram pass, the keys are read once); (2) if a bin overflowed (skewed /
+    // duplicate-heavy keys), the histogram path (varying-bit digit, per-tile counts,
+    // stable bin starts, big-bin list) redoes the L1 pass — its kernels are gated on
+    // the overflow word and exit at once otherwise.
+    uint32_t* ovf = sc.bigcount + 2;
+    e = cudaMemsetAsync(sc.bigcount, 0, 3 * sizeof(uint32_t), s);   // big-bin count, g2a ticket, overflow
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(sc.tot, 0, sizeof(uint32_t) * (size_t)L * nb1, s);   // bin cursors
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(sc.state, 0, sizeof(unsigned long long) * (size_t)L * nb1, s);   // look-back words
     if (e != cudaSuccess) return e;
-    e = l1_pass(keys, nullptr, sc.keys_a, sc.ids_a, n, L, spec, nb1, id_base, sc, sc.biglist, sc.bigcount, sc.num_sms, s,
-                true, /*stable=*/false);
-    if (e != cudaSuccess) return e;
+    const int64_t fix_tstride = (int64_t)nb1 * kG2BinCap;
+    {
+        timing_begin("group_scatter", s);
+        const int nst = 2;
+        const size_t smf = g1_scatter_smem(nb1, false, nst);
+        e = cudaFuncSetAttribute(g1_scatter<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smf);
+        if (e != cudaSuccess) return e;
+        const int grid = (int)std::min<int64_t>((int64_t)T * L, (int64_t)sc.num_sms * LSHB_SCATTER_CPS);
+        g1_scatter<true, false, true><<<grid, kSThreads, smf, s>>>(keys, nullptr, sc.keys_a, sc.ids_a, n, spec, nb1,
+                                                                   sc.tot, sc.binstart, T, L, id_base, nst, nullptr,
+                                                                   ovf, B1, W, fix_tstride, hint);
+        count_launch();
+        timing_end("group_scatter", s);
+        timing_begin("group_scan", s);
+        g1_fixscan<<<L, 1024, 0, s>>>(sc.tot, nb1, n, sc.binstart, spec, B1, W, ovf, hint);
+        count_launch();
+        timing_end("group_scan", s);
+    }
+    {
+        // fallback (gated on *ovf)
+        timing_begin("group_hist", s);
+        g1_hist<<<hist_grid(T, L, sc.num_sms), kG1Threads, nb1 * sizeof(uint32_t), s>>>(keys, n, spec, nb1, sc.hist, T, 1,
+                                                                                       W, B1, sc.vmask, ovf, L);
+        count_launch();
+        g0_spec<<<(L + 127) / 128, 128, 0, s>>>(sc.vmask, L, B1, 1, spec, ovf);
+        count_launch();
+        g1_hist<<<hist_grid(T, L, sc.num_sms), kG1Threads, nb1 * sizeof(uint32_t), s>>>(keys, n, spec, nb1, sc.hist, T, 2,
+                                                                                       W, B1, nullptr, ovf, L);
+        count_launch();
+        timing_end("group_hist", s);
+        timing_begin("group_scan", s);
+        const int64_t warps = (int64_t)L * ((nb1 + 31) / 32);
+        g1_scan<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(sc.hist, T, L, nb1, sc.tot, ovf);
+        count_launch();
+        g1_binstart<<<L, 1024, 0, s>>>(sc.tot, nb1, n, sc.binstart, sc.biglist, sc.bigcount, ovf);
+        count_launch();
+        timing_end("group_scan", s);
+        timing_begin("group_scatter", s);
+        const int nst = 2;
+        const size_t sm1 = g1_scatter_smem(nb1, false, nst);
+        e = cudaFuncSetAttribute(g1_scatter<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+        if (e != cudaSuccess) return e;
+        const int grid = (int)std::min<int64_t>((int64_t)T * L, (int64_t)sc.num_sms * LSHB_SCATTER_CPS);
+        g1_scatter<true, false><<<grid, kSThreads, sm1, s>>>(keys, nullptr, sc.keys_a, sc.ids_a, n, spec, nb1, sc.hist,
+                                                             sc.binstart, T, L, id_base, nst, ovf);
+        count_launch();
+        timing_end("group_scatter", s);
+    }
     timing_begin("group_sort", s);
     G2Args a;
     a.keys = sc.keys_a;
@@ -1478,6 +1610,8 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
     a.out = out;
     a.binheads = sc.tot;   // bin totals are dead after g1_binstart
     a.ticket = sc.bigcount + 1;
+    a.ovf = ovf;
+    a.fix_tstride = fix_tstride;
     const size_t smb = g2_big_smem();
     e = cudaFuncSetAttribute(g2_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb);
     if (e != cudaSuccess) return e;
@@ -1489,6 +1623,13 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
     g2a<<<bins, kG2aT, sizeof(G2aSmem), s>>>(a);   // sort every bin; ids, ukeys, offs out
     count_launch();
     timing_end("group_sort", s);
+    if (getenv("LSH_DEBUG_GROUP")) {
+        uint32_t hv[3];
+        cudaMemcpyAsync(hv, sc.bigcount, sizeof(hv), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        fprintf(stderr, "[group] n=%lld L=%d nb1=%d big=%u ticket=%u overflow=%u\n", (long long)n, L, nb1, hv[0], hv[1],
+                hv[2]);
+    }
     return cudaGetLastError();
 }
 

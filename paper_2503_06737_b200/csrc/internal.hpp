@@ -151,6 +151,7 @@ int group_bins(int64_t n, int key_width);
 size_t group_hist_words(int64_t n, int key_width);
 size_t group_spec_bytes();
 int group_rle_chunks(int64_t n);
+size_t group_key_slots(int64_t n, int key_width);   // per-table L1 output slots
 bool group_is_lsd(int key_width);
 cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_base, int key_width,
                          GroupScratch& sc, IndexDev& out, int* flags, cudaStream_t s);
