@@ -562,6 +562,7 @@ static lsh_status build_hcs_plan(lsh_handle* H) {
     hp.sgn = (const uint32_t*)(base + al(b_e) + al(b_p));
     hp.bp = (const uint16_t*)(base + al(b_e) + al(b_p) + al(b_s));
     hp.nblocks = nblocks;
+    hp.d = p->d;
     hp.bfirst = (const int32_t*)(base + al(b_e) + al(b_p) + al(b_s) + al(b_b));
     hp.wbins = (const uint8_t*)(base + al(b_e) + al(b_p) + al(b_s) + al(b_b) + al(b_f));
     H->hplan = hp;

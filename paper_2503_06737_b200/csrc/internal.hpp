@@ -87,6 +87,7 @@ struct HcsPlanDev {
     const uint8_t* wbins;    // [16][M12/16] bins of each warp (balanced by coordinate count)
     int nblocks;             // m / M12
     const int32_t* bfirst;   // [nblocks] index of each block's first entry
+    int64_t d;               // input width (= product of the modes: the slab plan has no padding)
 };
 
 struct DiscretizeDev {
