@@ -1021,7 +1021,7 @@ constexpr int kG2aIPT = LSHB_G2_IPT;
 constexpr int kG2aCap = kG2aT * kG2aIPT;      // 1280 items
 constexpr int kG2aD = LSHB_G2_D;               // digit bits (2^D counters)
 constexpr int kG2aCW = 1 << (kG2aD - 1);       // counter words (two u16 counters each)
-constexpr int kG2aLong = 64;                   // longest segment ranked item by item
+constexpr int kG2aLong = 8;                    // longest segment ranked item by item (O(s^2))
 constexpr int kG2aLongMax = kG2aCap / kG2aLong;
 static_assert(kG2aCap == kG2BinCap, "big-bin threshold");
 
@@ -1066,10 +1066,51 @@ struct __align__(16) G2aSmem {
 
 // Bitonic sort of the items at [s0, s0 + len) of S by (key, id): fin[p] = final
 // position of the item at p, bit 15 = bucket head.
-__device__ void g2a_long_segment(G2aSmem& S, uint32_t s0, uint32_t len, uint16_t* perm, uint16_t* fin) {
+// All segments longer than kG2aLong (duplicate-heavy codes) in ONE bitonic network:
+// their items (the union of the ranges S.lseg[0..nl), s0 << 16 | len) sorted by
+// (key, id); since distinct segments hold distinct digits (key ranges), the j-th item
+// of the sorted union belongs at the j-th position of the union in increasing order.
+// fin[p] = final position of the item at p, bit 15 = bucket head.  S.lseg is sorted
+// by s0 in place; `off` [kG2aLongMax + 1] receives the ranges' prefix lengths.
+__device__ void g2a_long_union(G2aSmem& S, uint32_t nl, uint16_t* perm, uint16_t* fin, uint32_t* off) {
+    // order the ranges by start (nl <= kG2aLongMax): rank by count of smaller starts
+    uint32_t mine[2];
+    int nm = 0;
+    for (uint32_t g = threadIdx.x; g < nl; g += kG2aT) {
+        uint32_t r = 0;
+        const uint32_t v = S.lseg[g];
+        for (uint32_t h = 0; h < nl; ++h) r += S.lseg[h] < v ? 1u : 0u;
+        mine[nm++] = (r << 16) | g;
+    }
+    cbar();
+    uint32_t tmp[2];
+    for (int q = 0; q < nm; ++q) tmp[q] = S.lseg[mine[q] & 0xffffu];
+    cbar();
+    for (int q = 0; q < nm; ++q) S.lseg[mine[q] >> 16] = tmp[q];
+    cbar();
+    if (threadIdx.x == 0) {
+        uint32_t acc = 0;
+        for (uint32_t g = 0; g < nl; ++g) {
+            off[g] = acc;
+            acc += S.lseg[g] & 0xffffu;
+        }
+        off[nl] = acc;
+    }
+    cbar();
+    const int total = (int)off[nl];
     int P = 1;
-    while (P < (int)len) P <<= 1;
-    for (int i = threadIdx.x; i < P; i += kG2aT) perm[i] = (uint16_t)(i < (int)len ? s0 + i : 0xffffu);
+    while (P < total) P <<= 1;
+    // position of the j-th union item (binary search over the range offsets)
+    auto upos = [&](int j) {
+        uint32_t lo = 0, hi = nl;   // last range with off <= j
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (off[mid] <= (uint32_t)j) lo = mid;
+            else hi = mid;
+        }
+        return (S.lseg[lo] >> 16) + ((uint32_t)j - off[lo]);
+    };
+    for (int i = threadIdx.x; i < P; i += kG2aT) perm[i] = (uint16_t)(i < total ? upos(i) : 0xffffu);
     cbar();
     auto less = [&](uint16_t x, uint16_t y) {   // pads (0xffff) sort last
         if (x == 0xffffu) return false;
@@ -1091,10 +1132,10 @@ __device__ void g2a_long_segment(G2aSmem& S, uint32_t s0, uint32_t len, uint16_t
             cbar();
         }
     }
-    for (int j = threadIdx.x; j < (int)len; j += kG2aT) {
+    for (int j = threadIdx.x; j < total; j += kG2aT) {
         const uint16_t pj = perm[j];
         const bool head = j == 0 || S.sk[perm[j - 1]] != S.sk[pj];
-        fin[pj] = (uint16_t)((s0 + j) | (head ? 0x8000u : 0u));
+        fin[pj] = (uint16_t)(upos(j) | (head ? 0x8000u : 0u));
     }
     cbar();
 }
@@ -1275,9 +1316,11 @@ __device__ __forceinline__ void g2_bin(const G2Args& a, G2aSmem& S, int t, int b
     const uint32_t nl = S.nlong;   // complete: appended before the last barrier
     if (nl) {
         // duplicate-heavy segments: bitonic sort by (key, id) in the (free) counter area
+        // counter area (8 KB): perm [<= 2048] u16 | fin [kG2aCap] u16 | off [<= 161] u32
+        static_assert(2048 * 2 + kG2aCap * 2 + (kG2aLongMax + 1) * 4 <= kG2aCW * 4, "long-segment scratch");
         uint16_t* perm = reinterpret_cast<uint16_t*>(S.cnt);
-        uint16_t* fin = perm + 2 * kG2aCap;
-        for (uint32_t g = 0; g < nl; ++g) g2a_long_segment(S, S.lseg[g] >> 16, S.lseg[g] & 0xffffu, perm, fin);
+        uint16_t* fin = perm + 2048;
+        g2a_long_union(S, nl, perm, fin, reinterpret_cast<uint32_t*>(fin + kG2aCap));
 #pragma unroll
         for (int j = 0; j < kG2aIPT; ++j) {
             const int i = u + j * kG2aT;
