@@ -446,9 +446,14 @@ def run_ours(args):
         #   dram  = ncu dram__bytes_read + dram__bytes_write of THIS build (committed
         #           capture, profiles/round2/ncu_summary.json), else null.
         narrow = (not h.e2lsh) and cfg.K <= 22
+        ovf_hist = (not narrow) and h.group_path() > 0
+        # group_hist: narrow keys read the keys three times (varying-bit mask, then one
+        # histogram per LSD pass); wide keys take the fixed-capacity L1 scatter, which needs
+        # no histogram: their hist kernels are the overflow fallback, gated off (0 bytes)
+        # unless a bin overflowed (ovf_hist below, from the build's own overflow word)
         io = {
             "sketch": (4 * cfg.d + 8 * cfg.L) * n_local,
-            "group_hist": 8 * Ln,
+            "group_hist": 24 * Ln if narrow else (16 * Ln if ovf_hist else 0),
             "group_scatter": (20 + 24) * Ln if narrow else 20 * Ln,
             "group_sort": (8 * Ln + 12 * nb_total) if narrow else (12 * Ln + 4 * Ln + 12 * nb_total),
         }
@@ -499,6 +504,8 @@ def run_ours(args):
         "roofline": roof,
         "step_roofline": step_roof,
         "roofline_kernels": kinfo,
+        "grouping_path": (None if dense else ("LSD (narrow keys)" if ((not h.e2lsh) and cfg.K <= 22) else
+                          ("histogram (bin overflow)" if h.group_path() > 0 else "fixed-capacity L1 scatter"))),
         "kernel_ms_per_step": kernel_ms,
         "cpu_baseline": cpu,
         "parity": par,

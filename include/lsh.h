@@ -235,6 +235,15 @@ lsh_status lsh_get_params(const lsh_handle* h, int32_t what, int32_t mode, void*
  * (LSH_EOVERFLOW if any E2LSH code left int32 since the last lsh_check). */
 lsh_status lsh_check(const lsh_handle* h);
 
+/* Grouping path of the handle's wide-key builds (E2LSH fingerprints, SRP with K > 22),
+ * DESIGN.md §7 K3; diagnostics only (both paths give the same canonical index, B11).
+ * Synchronises the handle's device.  *path = 0: the fixed-capacity L1 scatter (keys
+ * read once, no histogram pass); > 0: a recent build overflowed a bin (duplicate-heavy
+ * codes) and builds currently take the histogram path (the value counts down over the
+ * next builds).  Narrow keys always take the LSD path (*path = 0).  LSH_ESTATE if
+ * h or path is NULL. */
+lsh_status lsh_group_path(const lsh_handle* h, int32_t* path);
+
 const char* lsh_strerror(lsh_status s);
 const char* lsh_last_cuda_error(void);
 

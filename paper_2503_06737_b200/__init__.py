@@ -69,6 +69,7 @@ def lib() -> ctypes.CDLL:
         "lsh_export_host": (i32, [P(lsh_params), i32, i32, vp, P(sz)]),
         "lsh_get_params": (i32, [vp, i32, i32, vp, P(sz)]),
         "lsh_check": (i32, [vp]),
+        "lsh_group_path": (i32, [vp, P(i32)]),
         "lsh_strerror": (ctypes.c_char_p, [i32]),
         "lsh_last_cuda_error": (ctypes.c_char_p, []),
         "lsh_launch_count": (u64, []),
@@ -370,6 +371,13 @@ class LSH:
         _check(lib().lsh_get_params(self._h, EXPORT[what], mode, buf.ctypes.data_as(ctypes.c_void_p),
                                     ctypes.byref(sz)), "lsh_get_params")
         return buf
+
+    def group_path(self):
+        """Grouping path of the wide-key builds (lsh_group_path): 0 = fixed-capacity L1
+        scatter, > 0 = histogram path after a bin overflow."""
+        v = ctypes.c_int32(0)
+        _check(lib().lsh_group_path(self._h, ctypes.byref(v)), "lsh_group_path")
+        return int(v.value)
 
     def check(self):
         """Synchronise and raise LshError(LSH_EOVERFLOW) if a code left int32."""

@@ -23,8 +23,10 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 VARIANT_FLAGS = {"b11": ["-DLSHB_G2_IPT=5", "-DLSHB_G2_D=11", "-DLSHB_L1_AVG=512"],
                  # (C4: 4096-key tiles, 2 scatter CTAs per SM — E2LSH scatter 0.44 -> 0.92 ms
                  #  (shorter runs, more partial sectors), SRP 1.34 -> 1.22 ms — not kept)
-                 "t4k": ["-DLSHB_G1_TILE=4096", "-DLSHB_SCATTER_CPS=2"]}
-
+                 "t4k": ["-DLSHB_G1_TILE=4096", "-DLSHB_SCATTER_CPS=2"],
+                 # g2a CTA shape (C4 group_sort, round 2): 128 threads x 6 CTAs/SM 0.86 ms,
+                 # x 7 0.88 ms; 256 x 4 0.87 ms, x 5 0.79 ms (the default), x 6 0.79 ms (spills)
+                 "g128": ["-DLSHB_G2_T=128", "-DLSHB_G2_CPS=6"]}
 
 def nvcc() -> str:
     for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):

@@ -747,6 +747,16 @@ extern "C" lsh_status lsh_check(const lsh_handle* h) {
     return LSH_OK;
 }
 
+extern "C" lsh_status lsh_group_path(const lsh_handle* h, int32_t* path) {
+    if (!h || !path) return LSH_ESTATE;
+    CK(cudaSetDevice(h->device));
+    CK(cudaDeviceSynchronize());
+    int flags[2] = {0, 0};
+    CK(cudaMemcpy(flags, h->d_flags, sizeof(flags), cudaMemcpyDeviceToHost));
+    *path = flags[1];
+    return LSH_OK;
+}
+
 // ---------------------------------------------------------------------------
 // hashing
 // ---------------------------------------------------------------------------

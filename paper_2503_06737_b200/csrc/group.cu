@@ -43,8 +43,14 @@ constexpr int kG1Threads = 256;
 constexpr int kG2Threads = 512;
 constexpr int kG2Warps = kG2Threads / 32;       // 16
 constexpr int kG2Cap = 4096;                    // run-length-encoding chunk (narrow keys)
+#ifndef LSHB_G2_T
+#define LSHB_G2_T 256    // threads of the per-bin sort CTA (g2a)
+#endif
 #ifndef LSHB_G2_IPT
-#define LSHB_G2_IPT 10   // items per thread of the per-bin sort (g2a): cap 128 * IPT
+#define LSHB_G2_IPT (1280 / LSHB_G2_T)   // items per thread of g2a: bin capacity T * IPT = 1280
+#endif
+#ifndef LSHB_G2_CPS
+#define LSHB_G2_CPS (LSHB_G2_T == 128 ? 6 : 5)   // g2a CTAs per SM (launch bound)
 #endif
 #ifndef LSHB_G2_D
 #define LSHB_G2_D 12     // counting-sort digit bits inside a bin
@@ -52,7 +58,7 @@ constexpr int kG2Cap = 4096;                    // run-length-encoding chunk (na
 #ifndef LSHB_L1_AVG
 #define LSHB_L1_AVG 1024 // L1 bins hold at most this many keys on average
 #endif
-constexpr int kG2BinCap = 128 * LSHB_G2_IPT;    // largest L1 bin sorted in shared memory (g2a)
+constexpr int kG2BinCap = LSHB_G2_T * LSHB_G2_IPT;    // largest L1 bin sorted in shared memory (g2a)
 
 size_t group_tiles(int64_t n) { return (size_t)((n + kG1Tile - 1) / kG1Tile); }
 
@@ -431,9 +437,8 @@ __global__ void __launch_bounds__(kSThreads, LSHB_SCATTER_CPS)
     }
     uint64_t* bars = reinterpret_cast<uint64_t*>(g1_dsm);                                  // [nst]
     uint64_t* rk = reinterpret_cast<uint64_t*>(g1_dsm + 64);                               // [nst][4096]
-    uint16_t* sp = reinterpret_cast<uint16_t*>(rk + (size_t)nst * kG1Tile);                // staged item
-    uint16_t* sd = sp + kG1Tile;                                                           // staged digit
-    uint32_t* gpos = reinterpret_cast<uint32_t*>(sd + kG1Tile);                            // [nb1]
+    uint32_t* sp = reinterpret_cast<uint32_t*>(rk + (size_t)nst * kG1Tile);                // staged item | digit << 16
+    uint32_t* gpos = sp + kG1Tile;                                                         // [nb1] global - local start
     uint32_t* loc = gpos + nb1;                                                            // [nb1]
     uint16_t* wrun = reinterpret_cast<uint16_t*>(loc + nb1);                               // [kSWarps][nb1]
     __shared__ uint32_t ws[32];
@@ -582,24 +587,30 @@ __global__ void __launch_bounds__(kSThreads, LSHB_SCATTER_CPS)
             }
         }
         uint32_t ex = block_excl_scan<kSThreads>(mysum, ws, nullptr);
+        // digit starts (loc) and the tile's global run starts; FIX: the bin-cursor atomics
+        // are issued here and their results consumed only after the placement below, so
+        // their latency overlaps it.  gpos[d] = global start - local start (pos = gpos + p);
+        // an overflowed bin gets 0x80000000 (pos out of range: skipped, redone by the
+        // fallback)
+        uint32_t gj[4], lj[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int d = threadIdx.x * DPT + j;
+            gj[j] = 0u;
+            lj[j] = ex;
             if (j < DPT && d < nb1) {
                 const uint32_t c = loc[d];
                 loc[d] = ex;
                 ex += c;
                 if constexpr (FIX) {
-                    uint32_t g = 0xffffffffu;
-                    if (c) {
-                        const uint32_t b0 = atomicAdd(const_cast<uint32_t*>(hist) + (int64_t)t * nb1 + d, c);
-                        if (b0 + c <= (uint32_t)kG2BinCap) g = (uint32_t)d * kG2BinCap + b0;
-                        else atomicOr(ovf, 1u);
+                    gj[j] = c ? atomicAdd(const_cast<uint32_t*>(hist) + (int64_t)t * nb1 + d, c) : 0u;
+                    lj[j] |= c ? 0u : 0x80000000u;   // no items: nothing to place
+                    if (c && gj[j] + c > (uint32_t)kG2BinCap) {
+                        atomicOr(ovf, 1u);
+                        lj[j] |= 0x80000000u;
                     }
-                    gpos[d] = g;
                 } else {
-                    gpos[d] = STABLE ? gp[j]
-                                     : binstart[(int64_t)t * (nb1 + 1) + d] + hist[((int64_t)t * T + tile) * nb1 + d];
+                    gj[j] = STABLE ? gp[j] : binstart[(int64_t)t * (nb1 + 1) + d] + hist[((int64_t)t * T + tile) * nb1 + d];
                 }
             }
         }
@@ -610,16 +621,24 @@ __global__ void __launch_bounds__(kSThreads, LSHB_SCATTER_CPS)
             if (i < cnt) {
                 const uint32_t dg = slot[r] >> 16;
                 const uint32_t p = loc[dg] + (STABLE ? (uint32_t)wrun[warp * nb1 + dg] : 0u) + (slot[r] & 0xffffu);
-                sp[p] = (uint16_t)i;
-                sd[p] = (uint16_t)dg;
+                sp[p] = (uint32_t)i | (dg << 16);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int d = threadIdx.x * DPT + j;
+            if (j < DPT && d < nb1) {
+                if (FIX && (lj[j] & 0x80000000u)) gpos[d] = 0x80000000u;
+                else gpos[d] = (FIX ? (uint32_t)d * kG2BinCap + gj[j] : gj[j]) - lj[j];
             }
         }
         __syncthreads();
+        const uint32_t olim = (uint32_t)(FIX ? ostride : n);
         for (int p = threadIdx.x; p < cnt; p += kSThreads) {
-            const uint32_t i = sp[p], dg = sd[p];
-            if (FIX && gpos[dg] == 0xffffffffu) continue;   // overflowed bin: the fallback redoes it
-            const uint32_t pos = gpos[dg] + ((uint32_t)p - loc[dg]);
-            if (LSHB_OK(pos < (uint32_t)(FIX ? ostride : n) && i < (uint32_t)cnt)) {
+            const uint32_t v = sp[p], i = v & 0xffffu, dg = v >> 16;
+            const uint32_t pos = gpos[dg] + (uint32_t)p;
+            if (FIX && pos >= olim) continue;   // overflowed bin: the fallback redoes it
+            if (LSHB_OK(pos < olim && i < (uint32_t)cnt)) {
                 kout[tb + pos] = kr[i];
                 iout[tb + pos] = IMPLICIT_IDS ? id_base + (uint32_t)(tile * kG1Tile) + i : __ldg(ir + i);
             }
@@ -1015,7 +1034,7 @@ __global__ void __launch_bounds__(kG2Threads) g2_big(G2Args a) {
 //       its table (dynamic ticket order); warp 0 looks back while the others write
 //       the ids, then ukeys / offs are written at their final, compacted positions.
 // ---------------------------------------------------------------------------
-constexpr int kG2aT = 128;
+constexpr int kG2aT = LSHB_G2_T;
 constexpr int kG2aW = kG2aT / 32;
 constexpr int kG2aIPT = LSHB_G2_IPT;
 constexpr int kG2aCap = kG2aT * kG2aIPT;      // 1280 items
@@ -1028,7 +1047,7 @@ static_assert(kG2aCap == kG2BinCap, "big-bin threshold");
 // Barrier of the per-bin sort: named barrier 1 over its 128 sorting threads (a
 // persistent variant with a producer warp that never joins it was measured slower:
 // C4 g2 1.25 vs 0.91 ms — fewer CTAs per SM hide less of the sort's own latency).
-__device__ __forceinline__ void cbar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void cbar() { asm volatile("bar.sync 1, %0;" ::"n"(kG2aT) : "memory"); }
 __device__ __forceinline__ void g_mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(g_smem_u32(bar)) : "memory");
 }
@@ -1045,7 +1064,7 @@ __device__ __forceinline__ uint32_t cblock_excl_scan(uint32_t v, uint32_t* ws, u
     cbar();
     uint32_t before = 0, all = 0;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
+    for (int w = 0; w < kG2aW; ++w) {
         const uint32_t c = ws[w];
         before += w < warp ? c : 0u;
         all += c;
@@ -1058,11 +1077,13 @@ __device__ __forceinline__ uint32_t cblock_excl_scan(uint32_t v, uint32_t* ws, u
 struct __align__(16) G2aSmem {
     uint64_t sk[kG2aCap];
     uint32_t si[kG2aCap];
-    uint32_t cnt[kG2aCW];   // digit counters -> digit starts -> long-segment scratch
+    uint32_t cnt[kG2aCW];   // digit counters -> digit starts -> final positions (fin) + long-segment scratch
+    uint32_t wl[kG2aCap];   // short-segment worklist: p | s0 << 11 | len << 22
     uint32_t ws[kG2aW];
     uint32_t lseg[kG2aLongMax];
-    uint32_t nlong, heads;
+    uint32_t nlong, heads, nwl;
 };
+static_assert(kG2aCap <= 2048 && kG2aLong < 1024, "worklist packing");
 
 // Bitonic sort of the items at [s0, s0 + len) of S by (key, id): fin[p] = final
 // position of the item at p, bit 15 = bucket head.
@@ -1176,32 +1197,24 @@ __device__ void g2a_big_emit(const G2Args& a, int t, int bin, int64_t lo, int le
     }
 }
 
-// Sort one L1 bin of len <= kG2aCap items (keys src_k[0..len), ids src_i[0..len)) in
-// shared memory and emit its ids, ukeys and offs (module comment above).  Executed by
-// the 128 threads of the CTA (named barrier 1); `release` (nullable): mbarrier arrived
-// on by thread 0 once the items are in registers (a source stage may then be refilled).
+// Sort one L1 bin of len <= kG2aCap items (keys kr, ids ir: item u + j * kG2aT of the
+// bin in register j, already loaded by the caller) in shared memory and emit its ids,
+// ukeys and offs (module comment above).  Executed by the kG2aT threads of the CTA
+// (named barrier 1).
 __device__ __forceinline__ void g2_bin(const G2Args& a, G2aSmem& S, int t, int bin, int64_t lo, int len,
-                                       const uint64_t* src_k, const uint32_t* src_i, uint64_t* release,
+                                       const uint64_t (&kr)[kG2aIPT], const uint32_t (&ir)[kG2aIPT],
                                        uint32_t* s_base_p) {
     const int u = threadIdx.x, lane = u & 31, wu = u >> 5;
     const int nb1 = a.nb1;
     const int64_t n = a.n;
-    uint64_t kr[kG2aIPT];
-    uint32_t ir[kG2aIPT], dr[kG2aIPT];
-#pragma unroll
-    for (int j = 0; j < kG2aIPT; ++j) {
-        const int i = u + j * kG2aT;
-        if (i < len) {
-            kr[j] = src_k[i];
-            ir[j] = src_i[i];
-        }
-    }
+    uint32_t dr[kG2aIPT];
     {
         uint4* c4 = reinterpret_cast<uint4*>(S.cnt);
         for (int w = u; w < kG2aCW / 4; w += kG2aT) c4[w] = make_uint4(0u, 0u, 0u, 0u);
         if (u == 0) {
             S.nlong = 0u;
             S.heads = 0u;
+            S.nwl = 0u;
         }
     }
     const L1Spec sp = a.spec[t];
@@ -1210,7 +1223,6 @@ __device__ __forceinline__ void g2_bin(const G2Args& a, G2aSmem& S, int t, int b
     const int D = min(kG2aD, hb), sh = hb - D;
     const uint32_t dmask = (1u << D) - 1u;
     cbar();
-    if (release && u == 0) g_mbar_arrive(release);   // the stage is free for the next bin
     // (1) digit counts; the atomic's old value is the item's rank inside its digit
 #pragma unroll
     for (int j = 0; j < kG2aIPT; ++j) {
@@ -1264,13 +1276,16 @@ __device__ __forceinline__ void g2_bin(const G2Args& a, G2aSmem& S, int t, int b
     }
     cbar();
     // (2) place: an item alone in its digit is final; the others go to their digit's
-    // region (arbitrary order) and are ranked below.  dr: kDone, or (s0 << 16) | len
-    // for a short segment, or kLong | position for a long one
-    constexpr uint32_t kDone = 0xffffffffu, kLong = 0x80000000u;
+    // region (arbitrary order) and get their final position from fin[] below.  dr: kDone,
+    // or the item's placement position p
+    constexpr uint32_t kDone = 0xffffffffu;
+    uint16_t* fin = reinterpret_cast<uint16_t*>(S.cnt) + 2048;   // [kG2aCap]: final position | head << 15
     uint32_t heads = 0;
 #pragma unroll
     for (int j = 0; j < kG2aIPT; ++j) {
         const int i = u + j * kG2aT;
+        bool shortseg = false;
+        uint32_t wv = 0;
         if (i < len) {
             const uint32_t d = dr[j] >> 16, r = dr[j] & 0xffffu;
             const uint32_t w0 = S.cnt[d >> 1];
@@ -1278,29 +1293,45 @@ __device__ __forceinline__ void g2_bin(const G2Args& a, G2aSmem& S, int t, int b
             const uint32_t s1 = d == dmask ? (uint32_t)len
                                            : ((d & 1u) ? (S.cnt[(d + 1) >> 1] & 0xffffu) : (w0 >> 16));
             const uint32_t p = s0 + r;
-            if (!LSHB_OK(p < (uint32_t)len)) continue;
-            S.sk[p] = kr[j];
-            S.si[p] = ir[j];
-            if (s1 - s0 == 1) {
-                dr[j] = kDone;
-                ++heads;
-            } else if (s1 - s0 <= (uint32_t)kG2aLong) {
-                dr[j] = (s0 << 16) | (s1 - s0);
+            if (LSHB_OK(p < (uint32_t)len)) {
+                S.sk[p] = kr[j];
+                S.si[p] = ir[j];
+                if (s1 - s0 == 1) {
+                    dr[j] = kDone;
+                    ++heads;
+                } else {
+                    dr[j] = p;
+                    if (s1 - s0 <= (uint32_t)kG2aLong) {
+                        shortseg = true;
+                        wv = p | (s0 << 11) | ((s1 - s0) << 22);
+                    } else if (r == 0) {
+                        S.lseg[atomicAdd(&S.nlong, 1u)] = (s0 << 16) | (s1 - s0);
+                    }
+                }
             } else {
-                dr[j] = kLong | p;
-                if (r == 0) S.lseg[atomicAdd(&S.nlong, 1u)] = (s0 << 16) | (s1 - s0);
+                dr[j] = kDone;
             }
+        }
+        // warp-aggregated append of the short-segment members to the worklist
+        const uint32_t bal = __ballot_sync(0xffffffffu, shortseg);
+        if (bal) {
+            uint32_t wbase = 0;
+            if (lane == 0) wbase = atomicAdd(&S.nwl, (uint32_t)__popc(bal));
+            wbase = __shfl_sync(0xffffffffu, wbase, 0);
+            if (shortseg) S.wl[wbase + __popc(bal & lanemask_lt())] = wv;
         }
     }
     cbar();
-    // rank inside shared digits by (key, id); f = final position
-#pragma unroll
-    for (int j = 0; j < kG2aIPT; ++j) {
-        const int i = u + j * kG2aT;
-        if (i < len && dr[j] != kDone && !(dr[j] & kLong)) {
-            const uint32_t s0 = dr[j] >> 16, sl = dr[j] & 0xffffu;
-            const uint64_t k = kr[j];
-            const uint32_t id = ir[j];
+    // rank the worklist (members of digits shared by 2..kG2aLong items) by (key, id)
+    // inside their digit: fin[p] = final position, bit 15 = bucket head (no equal key of
+    // smaller id).  Reads only sk / si; every thread takes entries, not just the owners.
+    {
+        const uint32_t nw = S.nwl;
+        for (uint32_t w = u; w < nw; w += kG2aT) {
+            const uint32_t e = S.wl[w];
+            const uint32_t p = e & 0x7ffu, s0 = (e >> 11) & 0x7ffu, sl = e >> 22;
+            const uint64_t k = S.sk[p];
+            const uint32_t id = S.si[p];
             uint32_t f = s0, dup = 0;
             for (uint32_t qq = s0; qq < s0 + sl; ++qq) {
                 const uint64_t kq = S.sk[qq];
@@ -1309,26 +1340,26 @@ __device__ __forceinline__ void g2_bin(const G2Args& a, G2aSmem& S, int t, int b
                 f += (kq < k || eq_lt) ? 1u : 0u;
                 dup |= eq_lt ? 1u : 0u;
             }
-            dr[j] = f;   // < kCap: neither kDone nor kLong
-            heads += dup ^ 1u;
+            fin[p] = (uint16_t)(f | ((dup ^ 1u) << 15));
         }
     }
     const uint32_t nl = S.nlong;   // complete: appended before the last barrier
     if (nl) {
-        // duplicate-heavy segments: bitonic sort by (key, id) in the (free) counter area
-        // counter area (8 KB): perm [<= 2048] u16 | fin [kG2aCap] u16 | off [<= 161] u32
+        // duplicate-heavy segments: bitonic sort by (key, id) in the counter area:
+        // perm [<= 2048] u16 | fin [kG2aCap] u16 | off [<= 161] u32
         static_assert(2048 * 2 + kG2aCap * 2 + (kG2aLongMax + 1) * 4 <= kG2aCW * 4, "long-segment scratch");
         uint16_t* perm = reinterpret_cast<uint16_t*>(S.cnt);
-        uint16_t* fin = perm + 2048;
         g2a_long_union(S, nl, perm, fin, reinterpret_cast<uint32_t*>(fin + kG2aCap));
+    } else {
+        cbar();
+    }
 #pragma unroll
-        for (int j = 0; j < kG2aIPT; ++j) {
-            const int i = u + j * kG2aT;
-            if (i < len && dr[j] != kDone && (dr[j] & kLong)) {
-                const uint32_t fv = fin[dr[j] & 0xffffu];
-                dr[j] = fv & 0x7fffu;
-                heads += fv >> 15;
-            }
+    for (int j = 0; j < kG2aIPT; ++j) {
+        const int i = u + j * kG2aT;
+        if (i < len && dr[j] != kDone) {
+            const uint32_t fv = fin[dr[j]];
+            dr[j] = fv & 0x7fffu;
+            heads += fv >> 15;
         }
     }
     heads = __reduce_add_sync(0xffffffffu, heads);
@@ -1388,7 +1419,7 @@ __device__ __forceinline__ void g2_bin(const G2Args& a, G2aSmem& S, int t, int b
 }
 
 
-__global__ void __launch_bounds__(kG2aT, 6) g2a(G2Args a) {
+__global__ void __launch_bounds__(kG2aT, LSHB_G2_CPS) g2a(G2Args a) {
     extern __shared__ __align__(16) unsigned char g2a_dsm[];
     G2aSmem& S = *reinterpret_cast<G2aSmem*>(g2a_dsm);
     __shared__ uint32_t s_tick, s_base;
@@ -1401,17 +1432,38 @@ __global__ void __launch_bounds__(kG2aT, 6) g2a(G2Args a) {
     // tables interleaved: the CTAs in flight cover ~1/L of every table's bins, so each
     // table's look-back chain only has to advance a few bins per CTA lifetime
     const int t = (int)(s_tick % (uint32_t)a.L), bin = (int)(s_tick / (uint32_t)a.L);
+    // the fixed-capacity L1 layout's slots of this bin are loaded speculatively together
+    // with the bin's bounds (one memory round trip instead of two); if the histogram
+    // path produced the L1 output instead (*ovf != 0), the items are reloaded from it
+    const int u = threadIdx.x;
+    const int64_t fsrc = (int64_t)t * a.fix_tstride + (int64_t)bin * kG2aCap;
+    uint64_t kr[kG2aIPT];
+    uint32_t ir[kG2aIPT];
+#pragma unroll
+    for (int j = 0; j < kG2aIPT; ++j) {
+        kr[j] = a.keys[fsrc + u + j * kG2aT];
+        ir[j] = a.ids[fsrc + u + j * kG2aT];
+    }
     const uint32_t* bs = a.binstart + (int64_t)t * (nb1 + 1);
     const int64_t lo = bs[bin];
     const int len = (int)((int64_t)bs[bin + 1] - lo);
+    const bool fixed = a.ovf && *a.ovf == 0u;
     if (len > kG2aCap) {
         g2a_big_emit(a, t, bin, lo, len, &s_base);
         return;
     }
-    // source of the bin's items: the fixed-capacity L1 layout [t][bin][cap], or compact
-    const int64_t src = (a.ovf && *a.ovf == 0u) ? (int64_t)t * a.fix_tstride + (int64_t)bin * kG2aCap
-                                                : (int64_t)t * n + lo;
-    g2_bin(a, S, t, bin, lo, len, a.keys + src, a.ids + src, nullptr, &s_base);
+    if (!fixed) {
+        const int64_t src = (int64_t)t * n + lo;
+#pragma unroll
+        for (int j = 0; j < kG2aIPT; ++j) {
+            const int i = u + j * kG2aT;
+            if (i < len) {
+                kr[j] = a.keys[src + i];
+                ir[j] = a.ids[src + i];
+            }
+        }
+    }
+    g2_bin(a, S, t, bin, lo, len, kr, ir, &s_base);
 }
 
 // Run-length encoding of fully sorted keys (LSD path): chunk c = items
@@ -1666,13 +1718,6 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
     g2a<<<bins, kG2aT, sizeof(G2aSmem), s>>>(a);   // sort every bin; ids, ukeys, offs out
     count_launch();
     timing_end("group_sort", s);
-    if (getenv("LSH_DEBUG_GROUP")) {
-        uint32_t hv[3];
-        cudaMemcpyAsync(hv, sc.bigcount, sizeof(hv), cudaMemcpyDeviceToHost, s);
-        cudaStreamSynchronize(s);
-        fprintf(stderr, "[group] n=%lld L=%d nb1=%d big=%u ticket=%u overflow=%u\n", (long long)n, L, nb1, hv[0], hv[1],
-                hv[2]);
-    }
     return cudaGetLastError();
 }
 

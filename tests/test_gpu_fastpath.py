@@ -203,3 +203,4 @@ def test_c5_keys_only_sampled(scheme, parity_log):
     del X
     ref = _oracle(p, Xs)
     _check(p, ref, gk[:, rows], "C5/keys_only_sampled", parity_log)
+
