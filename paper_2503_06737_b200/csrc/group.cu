@@ -674,12 +674,16 @@ __device__ __forceinline__ uint32_t pget(const PT* p, int64_t r) {
     return p ? (uint32_t)p[r] : (uint32_t)r;
 }
 
-__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// Look-back state words: (flag << 32) | value in ONE aligned 64-bit word, so a reader
+// sees flag and value together (single-copy atomicity) and no other data is passed
+// through them: relaxed gpu-scope accesses suffice (st.release / ld.acquire compiled to
+// MEMBAR.ALL.GPU and an L1 invalidation, CCTL.IVALL, on the bin's critical path).
+__device__ __forceinline__ void st_state(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+__device__ __forceinline__ unsigned long long ld_state(const unsigned long long* p) {
     unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
 
@@ -691,19 +695,19 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 // `pre` (optional): the first round's values, loaded earlier by lookback_preload.
 __device__ __forceinline__ unsigned long long lookback_preload(const unsigned long long* st, int b) {
     const int idx = b - 1 - (int)(threadIdx.x & 31);
-    return idx >= 0 ? ld_acquire(st + idx) : (2ull << 32);
+    return idx >= 0 ? ld_state(st + idx) : (2ull << 32);
 }
 __device__ uint32_t chained_prefix_warp(unsigned long long* st, int b, uint32_t agg, bool published = false,
                                         const unsigned long long* pre = nullptr) {
     const int lane = threadIdx.x & 31;
-    if (lane == 0 && !published) st_release(st + b, ((b == 0 ? 2ull : 1ull) << 32) | agg);
+    if (lane == 0 && !published) st_state(st + b, ((b == 0 ? 2ull : 1ull) << 32) | agg);
     if (b == 0) return 0;
     uint32_t acc = 0;
     int j = b - 1;
     bool first = pre != nullptr;
     while (true) {
         const int idx = j - lane;
-        const unsigned long long v = first ? *pre : idx >= 0 ? ld_acquire(st + idx) : (2ull << 32);
+        const unsigned long long v = first ? *pre : idx >= 0 ? ld_state(st + idx) : (2ull << 32);
         first = false;
         const uint32_t f = (uint32_t)(v >> 32);
         const uint32_t incl = __ballot_sync(0xffffffffu, f == 2);
@@ -721,7 +725,7 @@ __device__ uint32_t chained_prefix_warp(unsigned long long* st, int b, uint32_t 
         if (incl) break;
         j -= 32;
     }
-    if (lane == 0) st_release(st + b, (2ull << 32) | (acc + agg));
+    if (lane == 0) st_state(st + b, (2ull << 32) | (acc + agg));
     return acc;
 }
 
@@ -1367,7 +1371,7 @@ __device__ __forceinline__ void g2_bin(const G2Args& a, G2aSmem& S, int t, int b
     cbar();   // every read of the digit regions is done; S.heads complete
     unsigned long long* st = a.state + (int64_t)t * nb1;
     const uint32_t agg = S.heads;
-    if (u == 0) st_release(st + bin, ((bin == 0 ? 2ull : 1ull) << 32) | agg);   // publish early
+    if (u == 0) st_state(st + bin, ((bin == 0 ? 2ull : 1ull) << 32) | agg);   // publish early
 #pragma unroll
     for (int j = 0; j < kG2aIPT; ++j) {
         const int i = u + j * kG2aT;

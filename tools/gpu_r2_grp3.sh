@@ -4,7 +4,7 @@ mkdir -p gpurun_out/r2
 export LSH_PARITY_LOG=gpurun_out/r2/parity_log_group.jsonl
 rm -f $LSH_PARITY_LOG
 timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fastpath.py tests/test_gpu_dist.py -q -m gpu -x -rf -k "group or index or knn or c4_keys or full_n or sharded" > gpurun_out/r2/pytest_group.log 2>&1; echo "rc=$?" >> gpurun_out/r2/pytest_group.log
-for W in "C4 CS_E2LSH" "C4 CS_SRP" "C5 HCS_E2LSH" "C2 CS_E2LSH"; do
+for W in "C4 CS_E2LSH" "C4 CS_SRP" "C5 HCS_E2LSH" "C2 CS_E2LSH" "C3 HCS_E2LSH"; do
   set -- $W
   timeout 600 python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --config $1 --scheme $2 > gpurun_out/r2/bench_${1}_${2}.log 2>&1
 done
