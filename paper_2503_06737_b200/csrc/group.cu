@@ -567,10 +567,15 @@ __global__ void __launch_bounds__(kSThreads, LSHB_SCATTER_CPS)
         }
         __syncthreads();
         // per digit: exclusive over warps (in place), tile count; exclusive over digits -> loc
+        // FIX: the bin-cursor atomics are issued as soon as the tile's digit counts are
+        // known and their results consumed only after the scan and the placement below,
+        // so their latency overlaps both
         uint32_t mysum = 0;
-        for (int j = 0; j < DPT; ++j) {
+        uint32_t gj[4] = {0u, 0u, 0u, 0u}, cj[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
             const int d = threadIdx.x * DPT + j;
-            if (d < nb1) {
+            if (j < DPT && d < nb1) {
                 uint32_t acc = 0;
                 if constexpr (STABLE) {
 #pragma unroll
@@ -582,33 +587,28 @@ __global__ void __launch_bounds__(kSThreads, LSHB_SCATTER_CPS)
                 } else {
                     acc = reinterpret_cast<const uint32_t*>(wrun)[d];
                 }
-                loc[d] = acc;
+                if constexpr (FIX) {
+                    if (acc) gj[j] = atomicAdd(const_cast<uint32_t*>(hist) + (int64_t)t * nb1 + d, acc);
+                }
+                cj[j] = acc;
                 mysum += acc;
             }
         }
         uint32_t ex = block_excl_scan<kSThreads>(mysum, ws, nullptr);
-        // digit starts (loc) and the tile's global run starts; FIX: the bin-cursor atomics
-        // are issued here and their results consumed only after the placement below, so
-        // their latency overlaps it.  gpos[d] = global start - local start (pos = gpos + p);
-        // an overflowed bin gets 0x80000000 (pos out of range: skipped, redone by the
-        // fallback)
-        uint32_t gj[4], lj[4];
+        // digit starts (loc) and the tile's global run starts: gpos[d] = global start -
+        // local start (pos = gpos + p); an overflowed bin gets 0x80000000 (pos out of
+        // range: skipped, redone by the fallback)
+        uint32_t lj[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int d = threadIdx.x * DPT + j;
-            gj[j] = 0u;
             lj[j] = ex;
             if (j < DPT && d < nb1) {
-                const uint32_t c = loc[d];
+                const uint32_t c = cj[j];
                 loc[d] = ex;
                 ex += c;
                 if constexpr (FIX) {
-                    gj[j] = c ? atomicAdd(const_cast<uint32_t*>(hist) + (int64_t)t * nb1 + d, c) : 0u;
                     lj[j] |= c ? 0u : 0x80000000u;   // no items: nothing to place
-                    if (c && gj[j] + c > (uint32_t)kG2BinCap) {
-                        atomicOr(ovf, 1u);
-                        lj[j] |= 0x80000000u;
-                    }
                 } else {
                     gj[j] = STABLE ? gp[j] : binstart[(int64_t)t * (nb1 + 1) + d] + hist[((int64_t)t * T + tile) * nb1 + d];
                 }
@@ -628,6 +628,10 @@ __global__ void __launch_bounds__(kSThreads, LSHB_SCATTER_CPS)
         for (int j = 0; j < 4; ++j) {
             const int d = threadIdx.x * DPT + j;
             if (j < DPT && d < nb1) {
+                if (FIX && cj[j] && gj[j] + cj[j] > (uint32_t)kG2BinCap) {   // bin overflow
+                    atomicOr(ovf, 1u);
+                    lj[j] |= 0x80000000u;
+                }
                 if (FIX && (lj[j] & 0x80000000u)) gpos[d] = 0x80000000u;
                 else gpos[d] = (FIX ? (uint32_t)d * kG2BinCap + gj[j] : gj[j]) - lj[j];
             }
@@ -1044,7 +1048,10 @@ constexpr int kG2aIPT = LSHB_G2_IPT;
 constexpr int kG2aCap = kG2aT * kG2aIPT;      // 1280 items
 constexpr int kG2aD = LSHB_G2_D;               // digit bits (2^D counters)
 constexpr int kG2aCW = 1 << (kG2aD - 1);       // counter words (two u16 counters each)
-constexpr int kG2aLong = 8;                    // longest segment ranked item by item (O(s^2))
+#ifndef LSHB_G2_LONG
+#define LSHB_G2_LONG 64
+#endif
+constexpr int kG2aLong = LSHB_G2_LONG;         // longest segment ranked item by item (O(s^2), worklist)
 constexpr int kG2aLongMax = kG2aCap / kG2aLong;
 static_assert(kG2aCap == kG2BinCap, "big-bin threshold");
 
