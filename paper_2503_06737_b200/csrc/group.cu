@@ -572,26 +572,35 @@ __global__ void __launch_bounds__(kSThreads, LSHB_SCATTER_CPS)
         // so their latency overlaps both
         uint32_t mysum = 0;
         uint32_t gj[4] = {0u, 0u, 0u, 0u}, cj[4] = {0u, 0u, 0u, 0u};
+        if constexpr (FIX) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int d = threadIdx.x * DPT + j;
-            if (j < DPT && d < nb1) {
-                uint32_t acc = 0;
-                if constexpr (STABLE) {
-#pragma unroll
-                    for (int ww = 0; ww < kSWarps; ++ww) {
-                        const uint32_t c = wrun[ww * nb1 + d];
-                        wrun[ww * nb1 + d] = (uint16_t)acc;
-                        acc += c;
-                    }
-                } else {
-                    acc = reinterpret_cast<const uint32_t*>(wrun)[d];
-                }
-                if constexpr (FIX) {
+            for (int j = 0; j < 4; ++j) {
+                const int d = threadIdx.x * DPT + j;
+                if (j < DPT && d < nb1) {
+                    const uint32_t acc = reinterpret_cast<const uint32_t*>(wrun)[d];
                     if (acc) gj[j] = atomicAdd(const_cast<uint32_t*>(hist) + (int64_t)t * nb1 + d, acc);
+                    cj[j] = acc;
+                    mysum += acc;
                 }
-                cj[j] = acc;
-                mysum += acc;
+            }
+        } else {
+            for (int j = 0; j < DPT; ++j) {
+                const int d = threadIdx.x * DPT + j;
+                if (d < nb1) {
+                    uint32_t acc = 0;
+                    if constexpr (STABLE) {
+#pragma unroll
+                        for (int ww = 0; ww < kSWarps; ++ww) {
+                            const uint32_t c = wrun[ww * nb1 + d];
+                            wrun[ww * nb1 + d] = (uint16_t)acc;
+                            acc += c;
+                        }
+                    } else {
+                        acc = reinterpret_cast<const uint32_t*>(wrun)[d];
+                    }
+                    loc[d] = acc;
+                    mysum += acc;
+                }
             }
         }
         uint32_t ex = block_excl_scan<kSThreads>(mysum, ws, nullptr);
@@ -604,7 +613,7 @@ __global__ void __launch_bounds__(kSThreads, LSHB_SCATTER_CPS)
             const int d = threadIdx.x * DPT + j;
             lj[j] = ex;
             if (j < DPT && d < nb1) {
-                const uint32_t c = cj[j];
+                const uint32_t c = FIX ? cj[j] : loc[d];
                 loc[d] = ex;
                 ex += c;
                 if constexpr (FIX) {
@@ -1287,16 +1296,15 @@ __device__ __forceinline__ void g2_bin(const G2Args& a, G2aSmem& S, int t, int b
     }
     cbar();
     // (2) place: an item alone in its digit is final; the others go to their digit's
-    // region (arbitrary order) and get their final position from fin[] below.  dr: kDone,
-    // or the item's placement position p
-    constexpr uint32_t kDone = 0xffffffffu;
+    // region (arbitrary order) and get their final position from fin[] below.  dr: kDone;
+    // a short-segment member's worklist entry p | s0 << 11 | len << 22; a long-segment
+    // member's p | kLongBit
+    constexpr uint32_t kDone = 0xffffffffu, kLongBit = 0x40000000u;
     uint16_t* fin = reinterpret_cast<uint16_t*>(S.cnt) + 2048;   // [kG2aCap]: final position | head << 15
-    uint32_t heads = 0;
+    uint32_t heads = 0, nshort = 0;
 #pragma unroll
     for (int j = 0; j < kG2aIPT; ++j) {
         const int i = u + j * kG2aT;
-        bool shortseg = false;
-        uint32_t wv = 0;
         if (i < len) {
             const uint32_t d = dr[j] >> 16, r = dr[j] & 0xffffu;
             const uint32_t w0 = S.cnt[d >> 1];
@@ -1310,26 +1318,34 @@ __device__ __forceinline__ void g2_bin(const G2Args& a, G2aSmem& S, int t, int b
                 if (s1 - s0 == 1) {
                     dr[j] = kDone;
                     ++heads;
+                } else if (s1 - s0 <= (uint32_t)kG2aLong) {
+                    dr[j] = p | (s0 << 11) | ((s1 - s0) << 22);
+                    ++nshort;
                 } else {
-                    dr[j] = p;
-                    if (s1 - s0 <= (uint32_t)kG2aLong) {
-                        shortseg = true;
-                        wv = p | (s0 << 11) | ((s1 - s0) << 22);
-                    } else if (r == 0) {
-                        S.lseg[atomicAdd(&S.nlong, 1u)] = (s0 << 16) | (s1 - s0);
-                    }
+                    dr[j] = p | kLongBit;
+                    if (r == 0) S.lseg[atomicAdd(&S.nlong, 1u)] = (s0 << 16) | (s1 - s0);
                 }
             } else {
                 dr[j] = kDone;
             }
         }
-        // warp-aggregated append of the short-segment members to the worklist
-        const uint32_t bal = __ballot_sync(0xffffffffu, shortseg);
-        if (bal) {
-            uint32_t wbase = 0;
-            if (lane == 0) wbase = atomicAdd(&S.nwl, (uint32_t)__popc(bal));
-            wbase = __shfl_sync(0xffffffffu, wbase, 0);
-            if (shortseg) S.wl[wbase + __popc(bal & lanemask_lt())] = wv;
+    }
+    {
+        // append the short-segment members to the worklist: one warp scan of the
+        // per-thread counts and one shared atomic per warp
+        uint32_t x = nshort;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        uint32_t wbase = 0;
+        if (lane == 31 && x) wbase = atomicAdd(&S.nwl, x);
+        wbase = __shfl_sync(0xffffffffu, wbase, 31) + x - nshort;
+#pragma unroll
+        for (int j = 0; j < kG2aIPT; ++j) {
+            const int i = u + j * kG2aT;
+            if (i < len && dr[j] != kDone && !(dr[j] & kLongBit)) S.wl[wbase++] = dr[j];
         }
     }
     cbar();
@@ -1368,7 +1384,7 @@ __device__ __forceinline__ void g2_bin(const G2Args& a, G2aSmem& S, int t, int b
     for (int j = 0; j < kG2aIPT; ++j) {
         const int i = u + j * kG2aT;
         if (i < len && dr[j] != kDone) {
-            const uint32_t fv = fin[dr[j]];
+            const uint32_t fv = fin[dr[j] & 0x7ffu];
             dr[j] = fv & 0x7fffu;
             heads += fv >> 15;
         }
