@@ -30,7 +30,11 @@ VARIANT_FLAGS = {"b11": ["-DLSHB_G2_IPT=5", "-DLSHB_G2_D=11", "-DLSHB_L1_AVG=512
                  # shared-digit segments ranked O(s^2) from the worklist up to this length,
                  # longer ones in one bitonic network (C5 / C3 HCS-E2LSH group_sort, round 2):
                  # 8: 1.88 / 0.249 ms, 32: 1.83 / 0.233, 64 (default): 1.75 / 0.229
-                 "l8": ["-DLSHB_G2_LONG=8"]}
+                 "l8": ["-DLSHB_G2_LONG=8"],
+                 # L1 bins of ~1950 keys (B1 = 9) at C4 (round 2): scatter 0.363 -> 0.322 ms but
+                 # g2a 0.69 -> 0.76 (256 x IPT 10, 4/SM, D 12) / 0.76 (3/SM, D 13) / 0.81 (512 x 5,
+                 # 2/SM, D 13); step 2.03 -> 2.06-2.12 ms: not kept
+                 "b9": ["-DLSHB_L1_AVG=2048", "-DLSHB_G2_T=256", "-DLSHB_G2_IPT=10", "-DLSHB_G2_CPS=3", "-DLSHB_G2_D=13"]}
 
 def nvcc() -> str:
     for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):

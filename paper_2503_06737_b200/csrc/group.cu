@@ -1062,6 +1062,11 @@ constexpr int kG2aCW = 1 << (kG2aD - 1);       // counter words (two u16 counter
 #endif
 constexpr int kG2aLong = LSHB_G2_LONG;         // longest segment ranked item by item (O(s^2), worklist)
 constexpr int kG2aLongMax = kG2aCap / kG2aLong;
+constexpr int kG2aP2 = kG2aCap <= 1024 ? 1024 : kG2aCap <= 2048 ? 2048 : 4096;   // bitonic width >= cap
+// digit counters, then (after the placement) the long-segment scratch:
+// perm [kG2aP2] u16 | fin [kG2aCap] u16 | off [kG2aLongMax + 1] u32
+constexpr int kG2aScratchW = (kG2aP2 * 2 + kG2aCap * 2 + (kG2aLongMax + 1) * 4 + 3) / 4;
+constexpr int kG2aCntW = kG2aCW > kG2aScratchW ? kG2aCW : kG2aScratchW;
 static_assert(kG2aCap == kG2BinCap, "big-bin threshold");
 
 // Barrier of the per-bin sort: named barrier 1 over its 128 sorting threads (a
@@ -1097,13 +1102,14 @@ __device__ __forceinline__ uint32_t cblock_excl_scan(uint32_t v, uint32_t* ws, u
 struct __align__(16) G2aSmem {
     uint64_t sk[kG2aCap];
     uint32_t si[kG2aCap];
-    uint32_t cnt[kG2aCW];   // digit counters -> digit starts -> final positions (fin) + long-segment scratch
-    uint32_t wl[kG2aCap];   // short-segment worklist: p | s0 << 11 | len << 22
+    uint32_t cnt[kG2aCntW];   // digit counters -> digit starts -> final positions (fin) + long-segment scratch
+    uint32_t wl[kG2aCap];   // short-segment worklist: p | s0 << 12 | len << 24
     uint32_t ws[kG2aW];
     uint32_t lseg[kG2aLongMax];
     uint32_t nlong, heads, nwl;
 };
-static_assert(kG2aCap <= 2048 && kG2aLong < 1024, "worklist packing");
+static_assert(kG2aCap <= 4096 && kG2aLong <= 127, "worklist packing");
+static_assert(kG2aLongMax <= kG2aT, "long segments: one per thread when ordering them");
 
 // Bitonic sort of the items at [s0, s0 + len) of S by (key, id): fin[p] = final
 // position of the item at p, bit 15 = bucket head.
@@ -1115,19 +1121,14 @@ static_assert(kG2aCap <= 2048 && kG2aLong < 1024, "worklist packing");
 // by s0 in place; `off` [kG2aLongMax + 1] receives the ranges' prefix lengths.
 __device__ void g2a_long_union(G2aSmem& S, uint32_t nl, uint16_t* perm, uint16_t* fin, uint32_t* off) {
     // order the ranges by start (nl <= kG2aLongMax): rank by count of smaller starts
-    uint32_t mine[2];
-    int nm = 0;
-    for (uint32_t g = threadIdx.x; g < nl; g += kG2aT) {
-        uint32_t r = 0;
-        const uint32_t v = S.lseg[g];
+    const uint32_t g = threadIdx.x;   // nl <= kG2aLongMax <= kG2aT: one range per thread
+    uint32_t r = 0, v = 0;
+    if (g < nl) {
+        v = S.lseg[g];
         for (uint32_t h = 0; h < nl; ++h) r += S.lseg[h] < v ? 1u : 0u;
-        mine[nm++] = (r << 16) | g;
     }
     cbar();
-    uint32_t tmp[2];
-    for (int q = 0; q < nm; ++q) tmp[q] = S.lseg[mine[q] & 0xffffu];
-    cbar();
-    for (int q = 0; q < nm; ++q) S.lseg[mine[q] >> 16] = tmp[q];
+    if (g < nl) S.lseg[r] = v;
     cbar();
     if (threadIdx.x == 0) {
         uint32_t acc = 0;
@@ -1297,10 +1298,10 @@ __device__ __forceinline__ void g2_bin(const G2Args& a, G2aSmem& S, int t, int b
     cbar();
     // (2) place: an item alone in its digit is final; the others go to their digit's
     // region (arbitrary order) and get their final position from fin[] below.  dr: kDone;
-    // a short-segment member's worklist entry p | s0 << 11 | len << 22; a long-segment
+    // a short-segment member's worklist entry p | s0 << 12 | len << 24; a long-segment
     // member's p | kLongBit
-    constexpr uint32_t kDone = 0xffffffffu, kLongBit = 0x40000000u;
-    uint16_t* fin = reinterpret_cast<uint16_t*>(S.cnt) + 2048;   // [kG2aCap]: final position | head << 15
+    constexpr uint32_t kDone = 0xffffffffu, kLongBit = 0x80000000u;
+    uint16_t* fin = reinterpret_cast<uint16_t*>(S.cnt) + kG2aP2;   // [kG2aCap]: final position | head << 15
     uint32_t heads = 0, nshort = 0;
 #pragma unroll
     for (int j = 0; j < kG2aIPT; ++j) {
@@ -1319,7 +1320,7 @@ __device__ __forceinline__ void g2_bin(const G2Args& a, G2aSmem& S, int t, int b
                     dr[j] = kDone;
                     ++heads;
                 } else if (s1 - s0 <= (uint32_t)kG2aLong) {
-                    dr[j] = p | (s0 << 11) | ((s1 - s0) << 22);
+                    dr[j] = p | (s0 << 12) | ((s1 - s0) << 24);
                     ++nshort;
                 } else {
                     dr[j] = p | kLongBit;
@@ -1356,7 +1357,7 @@ __device__ __forceinline__ void g2_bin(const G2Args& a, G2aSmem& S, int t, int b
         const uint32_t nw = S.nwl;
         for (uint32_t w = u; w < nw; w += kG2aT) {
             const uint32_t e = S.wl[w];
-            const uint32_t p = e & 0x7ffu, s0 = (e >> 11) & 0x7ffu, sl = e >> 22;
+            const uint32_t p = e & 0xfffu, s0 = (e >> 12) & 0xfffu, sl = (e >> 24) & 0x7fu;
             const uint64_t k = S.sk[p];
             const uint32_t id = S.si[p];
             uint32_t f = s0, dup = 0;
@@ -1373,8 +1374,7 @@ __device__ __forceinline__ void g2_bin(const G2Args& a, G2aSmem& S, int t, int b
     const uint32_t nl = S.nlong;   // complete: appended before the last barrier
     if (nl) {
         // duplicate-heavy segments: bitonic sort by (key, id) in the counter area:
-        // perm [<= 2048] u16 | fin [kG2aCap] u16 | off [<= 161] u32
-        static_assert(2048 * 2 + kG2aCap * 2 + (kG2aLongMax + 1) * 4 <= kG2aCW * 4, "long-segment scratch");
+        // perm [kG2aP2] u16 | fin [kG2aCap] u16 | off [kG2aLongMax + 1] u32
         uint16_t* perm = reinterpret_cast<uint16_t*>(S.cnt);
         g2a_long_union(S, nl, perm, fin, reinterpret_cast<uint32_t*>(fin + kG2aCap));
     } else {
@@ -1384,7 +1384,7 @@ __device__ __forceinline__ void g2_bin(const G2Args& a, G2aSmem& S, int t, int b
     for (int j = 0; j < kG2aIPT; ++j) {
         const int i = u + j * kG2aT;
         if (i < len && dr[j] != kDone) {
-            const uint32_t fv = fin[dr[j] & 0x7ffu];
+            const uint32_t fv = fin[dr[j] & 0xfffu];
             dr[j] = fv & 0x7fffu;
             heads += fv >> 15;
         }
