@@ -20,7 +20,7 @@ from bench import source_hash  # noqa: E402
 
 TIMING = [("sketch_kernel", "sketch"), ("sketch_chunked", "sketch"), ("sketch_hcs", "sketch"),
           ("g0_mask", "group_hist"), ("g0_spec", "group_hist"), ("g1_hist", "group_hist"),
-          ("g1_scan", "group_scan"), ("g1_binstart", "group_scan"), ("g1_scatter", "group_scatter"),
+          ("g1_scan", "group_scan"), ("g1_binstart", "group_scan"), ("g1_fixscan", "group_scan"), ("g1_scatter", "group_scatter"),
           ("g2_big", "group_sort"), ("g2a", "group_sort"), ("g3_rle", "group_sort"), ("lookup", "lookup"),
           ("dense_tc", "dense_gemm"), ("split3", "dense_gemm")]
 WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
