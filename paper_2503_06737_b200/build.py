@@ -25,7 +25,8 @@ VARIANT_FLAGS = {"b11": ["-DLSHB_G2_IPT=5", "-DLSHB_G2_D=11", "-DLSHB_L1_AVG=512
                  #  (shorter runs, more partial sectors), SRP 1.34 -> 1.22 ms — not kept)
                  "t4k": ["-DLSHB_G1_TILE=4096", "-DLSHB_SCATTER_CPS=2"],
                  # g2a CTA shape (C4 group_sort, round 2): 128 threads x 6 CTAs/SM 0.86 ms,
-                 # x 7 0.88 ms; 256 x 4 0.87 ms, x 5 0.79 ms (the default), x 6 0.79 ms (spills)
+                 # x 7 0.88 ms; 256 x 4 0.87 ms, x 5 0.79 ms (the default), x 6 0.79 ms (spills);
+                 # with the final g2a body: 256 x 5 0.683, 256 x 4 0.751, 128 x 8 0.830 ms
                  "g128": ["-DLSHB_G2_T=128", "-DLSHB_G2_CPS=6"],
                  # shared-digit segments ranked O(s^2) from the worklist up to this length,
                  # longer ones in one bitonic network (C5 / C3 HCS-E2LSH group_sort, round 2):
