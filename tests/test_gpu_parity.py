@@ -596,3 +596,25 @@ def test_fused_key_epilogue_equals_materialised(scheme, d, m, L, K, per_table):
     ref["band"] = parity.code_band(p, t, Xn) if lsh.is_e2lsh(p.scheme) else parity.srp_band(p, t, Xn)
     kr = parity.check_keys(p, ref, kf.view(np.uint64))
     assert kr["mismatch_outside_exempt"] == 0, kr
+
+
+def test_group_path_overflow_fallback_and_hint():
+    """Wide keys take the fixed-capacity L1 scatter (lsh_group_path 0) until a bin
+    overflows — here 30,000 identical points, one bucket per table — then the gated
+    histogram path redoes the grouping in the same build and the hint keeps the next
+    builds on it (path > 0); the index equals the oracle's grouping of the kernel's keys
+    on every build, whichever path ran (DESIGN.md §7 K3)."""
+    c = synth.CONFIGS["C2"]
+    p = _params(c, "CS_E2LSH")
+    h = _handle(p)
+    X = synth.rows(c, 0, c.n, device="cuda")
+    Xdup = X.clone()
+    Xdup[:30000] = X[0]
+    for step, (Xs, want) in enumerate([(X, 0), (Xdup, 1), (X, 1)]):
+        keys = h.hash(Xs, keys=True)["keys"].cpu().numpy()
+        idx = h.build_index(Xs, id_base=0)
+        torch.cuda.synchronize()
+        path = h.group_path()
+        assert (path > 0) == bool(want), (step, path)
+        _check_index(idx, lsh.group(keys), p.L)
+        idx.close()
