@@ -1229,21 +1229,13 @@ __device__ __forceinline__ void g2_bin(const G2Args& a, G2aSmem& S, int t, int b
     const int nb1 = a.nb1;
     const int64_t n = a.n;
     uint32_t dr[kG2aIPT];
-    {
-        uint4* c4 = reinterpret_cast<uint4*>(S.cnt);
-        for (int w = u; w < kG2aCW / 4; w += kG2aT) c4[w] = make_uint4(0u, 0u, 0u, 0u);
-        if (u == 0) {
-            S.nlong = 0u;
-            S.heads = 0u;
-            S.nwl = 0u;
-        }
-    }
+    // (the digit counters and S.nlong / S.heads / S.nwl were zeroed by the caller before
+    // its last barrier)
     const L1Spec sp = a.spec[t];
     // keys of the bin agree on every bit at or above the lowest L1 digit bit (hb)
     const int hb = sp.below == 0 ? 0 : 64 - __clzll((long long)sp.below);
     const int D = min(kG2aD, hb), sh = hb - D;
     const uint32_t dmask = (1u << D) - 1u;
-    cbar();
     // (1) digit counts; the atomic's old value is the item's rank inside its digit
 #pragma unroll
     for (int j = 0; j < kG2aIPT; ++j) {
@@ -1380,30 +1372,28 @@ __device__ __forceinline__ void g2_bin(const G2Args& a, G2aSmem& S, int t, int b
     } else {
         cbar();
     }
+    // final positions of the items of shared digits, written at once: every read of sk /
+    // si by the ranking is behind the last barrier, and the fin[] reads touch the counter
+    // area only
 #pragma unroll
     for (int j = 0; j < kG2aIPT; ++j) {
         const int i = u + j * kG2aT;
         if (i < len && dr[j] != kDone) {
             const uint32_t fv = fin[dr[j] & 0xfffu];
-            dr[j] = fv & 0x7fffu;
+            const uint32_t f = fv & 0x7fffu;
             heads += fv >> 15;
+            if (LSHB_OK(f < (uint32_t)len)) {
+                S.sk[f] = kr[j];
+                S.si[f] = ir[j];
+            }
         }
     }
     heads = __reduce_add_sync(0xffffffffu, heads);
     if (lane == 0) atomicAdd(&S.heads, heads);
-    cbar();   // every read of the digit regions is done; S.heads complete
+    cbar();   // the bin is sorted in sk / si; S.heads complete
     unsigned long long* st = a.state + (int64_t)t * nb1;
     const uint32_t agg = S.heads;
-    if (u == 0) st_state(st + bin, ((bin == 0 ? 2ull : 1ull) << 32) | agg);   // publish early
-#pragma unroll
-    for (int j = 0; j < kG2aIPT; ++j) {
-        const int i = u + j * kG2aT;
-        if (i < len && dr[j] != kDone && LSHB_OK(dr[j] < (uint32_t)len)) {
-            S.sk[dr[j]] = kr[j];
-            S.si[dr[j]] = ir[j];
-        }
-    }
-    cbar();
+    if (u == 0) st_state(st + bin, ((bin == 0 ? 2ull : 1ull) << 32) | agg);   // publish
     // (3) ids out (coalesced) while warp 0 looks back for the bin's first bucket number
     uint32_t* od = a.out.ids + (int64_t)t * n + lo;
     for (int p = u; p < len; p += kG2aT) __stcs(od + p, S.si[p]);
@@ -1455,6 +1445,16 @@ __global__ void __launch_bounds__(kG2aT, LSHB_G2_CPS) g2a(G2Args a) {
     // bins are numbered through a dynamic ticket, so every bin this CTA looks back at
     // belongs to a CTA that is already running: the look-back cannot stall
     if (threadIdx.x == 0) s_tick = atomicAdd(a.ticket, 1u);
+    {
+        // g2_bin's shared state, zeroed under the ticket's latency
+        uint4* c4 = reinterpret_cast<uint4*>(S.cnt);
+        for (int w = threadIdx.x; w < kG2aCW / 4; w += kG2aT) c4[w] = make_uint4(0u, 0u, 0u, 0u);
+        if (threadIdx.x == 0) {
+            S.nlong = 0u;
+            S.heads = 0u;
+            S.nwl = 0u;
+        }
+    }
     cbar();
     // tables interleaved: the CTAs in flight cover ~1/L of every table's bins, so each
     // table's look-back chain only has to advance a few bins per CTA lifetime
