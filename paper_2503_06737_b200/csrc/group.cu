@@ -402,9 +402,16 @@ __device__ __forceinline__ void g_bulk(void* dst, const void* src, uint32_t byte
 }
 }  // namespace
 
-constexpr int kSThreads = 512;
+#ifndef LSHB_SCATTER_T
+#define LSHB_SCATTER_T 512   // L1 scatter CTA threads
+#endif
+#ifndef LSHB_SCATTER_NST
+#define LSHB_SCATTER_NST 2   // L1 scatter tile ring stages
+#endif
+constexpr int kSThreads = LSHB_SCATTER_T;
+constexpr int kSMaxDPT = (2048 + kSThreads - 1) / kSThreads;   // digits per thread (nb1 <= 2048)
 constexpr int kSWarps = kSThreads / 32;
-constexpr int kSRounds = kG1Tile / kSThreads;   // 16
+constexpr int kSRounds = kG1Tile / kSThreads;   // 16 at 512 threads
 
 size_t g1_scatter_smem(int nb1, bool stable, int nst) {
     // ring, staged permutation + digit, offsets, counters (per warp if stable)
@@ -507,10 +514,10 @@ __global__ void __launch_bounds__(kSThreads, LSHB_SCATTER_CPS)
         // this tile's global run starts per digit.  Stable (LSD) passes: loads issued now,
         // consumed after the ranking (measured: SRP scatter 1.39 -> 1.34 ms); the wide-key
         // pass loads them after the scan (prefetching there measured slower, 0.45 -> 0.55 ms)
-        const int DPT = (nb1 + kSThreads - 1) / kSThreads;   // <= 4 (nb1 <= 2048)
-        uint32_t gp[4];
+        const int DPT = (nb1 + kSThreads - 1) / kSThreads;   // <= kSMaxDPT (nb1 <= 2048)
+        uint32_t gp[kSMaxDPT];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < kSMaxDPT; ++j) {
             const int d = threadIdx.x * DPT + j;
             gp[j] = (STABLE && j < DPT && d < nb1)
                         ? __ldg(binstart + (int64_t)t * (nb1 + 1) + d) + __ldg(hist + ((int64_t)t * T + tile) * nb1 + d)
@@ -571,10 +578,12 @@ __global__ void __launch_bounds__(kSThreads, LSHB_SCATTER_CPS)
         // known and their results consumed only after the scan and the placement below,
         // so their latency overlaps both
         uint32_t mysum = 0;
-        uint32_t gj[4] = {0u, 0u, 0u, 0u}, cj[4] = {0u, 0u, 0u, 0u};
+        uint32_t gj[kSMaxDPT], cj[kSMaxDPT];
+#pragma unroll
+        for (int j = 0; j < kSMaxDPT; ++j) gj[j] = cj[j] = 0u;
         if constexpr (FIX) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < kSMaxDPT; ++j) {
                 const int d = threadIdx.x * DPT + j;
                 if (j < DPT && d < nb1) {
                     const uint32_t acc = reinterpret_cast<const uint32_t*>(wrun)[d];
@@ -607,9 +616,9 @@ __global__ void __launch_bounds__(kSThreads, LSHB_SCATTER_CPS)
         // digit starts (loc) and the tile's global run starts: gpos[d] = global start -
         // local start (pos = gpos + p); an overflowed bin gets 0x80000000 (pos out of
         // range: skipped, redone by the fallback)
-        uint32_t lj[4];
+        uint32_t lj[kSMaxDPT];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < kSMaxDPT; ++j) {
             const int d = threadIdx.x * DPT + j;
             lj[j] = ex;
             if (j < DPT && d < nb1) {
@@ -634,7 +643,7 @@ __global__ void __launch_bounds__(kSThreads, LSHB_SCATTER_CPS)
             }
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < kSMaxDPT; ++j) {
             const int d = threadIdx.x * DPT + j;
             if (j < DPT && d < nb1) {
                 if (FIX && cj[j] && gj[j] + cj[j] > (uint32_t)kG2BinCap) {   // bin overflow
@@ -1583,7 +1592,7 @@ static cudaError_t l1_pass(const uint64_t* kin, const uint32_t* iin, uint64_t* k
     timing_end("group_scan", s);
     timing_begin("group_scatter", s);
     const bool ids = iin != nullptr;
-    int nst = 2;
+    int nst = LSHB_SCATTER_NST;
     const size_t sm1 = g1_scatter_smem(nb1, stable || ids, nst);
     const int64_t items = (int64_t)T * L;
     const int grid = (int)std::min<int64_t>(items, (int64_t)num_sms * LSHB_SCATTER_CPS);
@@ -1670,7 +1679,7 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
     const int64_t fix_tstride = (int64_t)nb1 * kG2BinCap;
     {
         timing_begin("group_scatter", s);
-        const int nst = 2;
+        const int nst = LSHB_SCATTER_NST;
         const size_t smf = g1_scatter_smem(nb1, false, nst);
         e = cudaFuncSetAttribute(g1_scatter<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smf);
         if (e != cudaSuccess) return e;
@@ -1705,7 +1714,7 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
         count_launch();
         timing_end("group_scan", s);
         timing_begin("group_scatter", s);
-        const int nst = 2;
+        const int nst = LSHB_SCATTER_NST;
         const size_t sm1 = g1_scatter_smem(nb1, false, nst);
         e = cudaFuncSetAttribute(g1_scatter<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
         if (e != cudaSuccess) return e;
