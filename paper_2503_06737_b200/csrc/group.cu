@@ -1403,10 +1403,12 @@ __device__ __forceinline__ void g2_bin(const G2Args& a, G2aSmem& S, int t, int b
     unsigned long long* st = a.state + (int64_t)t * nb1;
     const uint32_t agg = S.heads;
     if (u == 0) st_state(st + bin, ((bin == 0 ? 2ull : 1ull) << 32) | agg);   // publish
-    // (3) ids out (coalesced) while warp 0 looks back for the bin's first bucket number
+    // (3) ids out (coalesced, by warps 1..) while warp 0 looks back for the bin's first
+    // bucket number
     uint32_t* od = a.out.ids + (int64_t)t * n + lo;
-    for (int p = u; p < len; p += kG2aT) __stcs(od + p, S.si[p]);
-    if (u < 32) {
+    if (u >= 32) {
+        for (int p = u - 32; p < len; p += kG2aT - 32) __stcs(od + p, S.si[p]);
+    } else {
         const uint32_t pre = chained_prefix_warp(st, bin, agg, /*published=*/true);
         if (u == 0) *s_base_p = pre;
     }
