@@ -35,6 +35,9 @@ VARIANT_FLAGS = {"b11": ["-DLSHB_G2_IPT=5", "-DLSHB_G2_D=11", "-DLSHB_L1_AVG=512
                  # L1 bins of ~1950 keys (B1 = 9) at C4 (round 2): scatter 0.363 -> 0.322 ms but
                  # g2a 0.69 -> 0.76 (256 x IPT 10, 4/SM, D 12) / 0.76 (3/SM, D 13) / 0.81 (512 x 5,
                  # 2/SM, D 13); step 2.03 -> 2.06-2.12 ms: not kept
+                 # K1 keys-only loop, tables per unrolled iteration (C4 E2LSH / SRP sketch,
+                 # round 2): 1: 0.929 / 0.796 ms, 2 (default): 0.920 / 0.784, 4: 0.929 / 0.776
+                 "tu4": ["-DLSHB_SK_TUNROLL=4"],
                  # L1 scatter with 1024-thread CTAs (C4, round 2): E2LSH 0.364 -> 0.353 ms,
                  # SRP LSD passes 1.28 -> 1.34 ms: not kept
                  "s1024": ["-DLSHB_SCATTER_T=1024"],

@@ -29,11 +29,16 @@
 #include "discretize.cuh"
 #include "internal.hpp"
 
+#ifndef LSHB_SK_TUNROLL
+#define LSHB_SK_TUNROLL 2   // tables per iteration of a warp's keys-only loop
+#endif
+
 namespace lshb {
 namespace sk {
 
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
+constexpr int kTUnroll = LSHB_SK_TUNROLL;
 constexpr int CW = kSketchColWords;   // words per staged float4 column (4 coordinates x 32 points + pad)
 
 __device__ __forceinline__ float4 ldg_stream_f4(const float* p) {
@@ -253,7 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // reads it — a coordinate belongs to one bin, a bin to one table, a table to one
             // warp); then every bin is the sum of two staged words through `pairs`
             // (branch-free; a missing one reads the zero slot).  Two tables per iteration.
-#pragma unroll 2
+#pragma unroll kTUnroll
             for (int t = warp; t < L; t += kWarps) {
                 float acc[KT];
                 {
