@@ -10,7 +10,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $F/smoke.log 2>
 unset LSH_PARITY_LOG
 for W in "C4 CS_E2LSH build" "C4 CS_SRP build" "C5 HCS_E2LSH build"; do
   set -- $W
-  ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "profile/" -o /tmp/${1}_${2}_full \
+  ncu -f --set full --clock-control none --import-source on --nvtx --nvtx-include "profile/" -o /tmp/${1}_${2}_full \
       python tools/prof_hash.py --config $1 --scheme $2 --op $3 --reps 1 > $F/prof/ncu_${1}_${2}.log 2>&1
 done
 python tools/summarize_r2.py $F/prof C4:CS_E2LSH=/tmp/C4_CS_E2LSH_full.ncu-rep C4:CS_SRP=/tmp/C4_CS_SRP_full.ncu-rep \
