@@ -38,6 +38,9 @@ VARIANT_FLAGS = {"b11": ["-DLSHB_G2_IPT=5", "-DLSHB_G2_D=11", "-DLSHB_L1_AVG=512
                  # K1 keys-only loop, tables per unrolled iteration (C4 E2LSH / SRP sketch,
                  # round 2): 1: 0.929 / 0.796 ms, 2 (default): 0.920 / 0.784, 4: 0.929 / 0.776
                  "tu4": ["-DLSHB_SK_TUNROLL=4"],
+                 # g2a digit bits below the L1 digit (C4 group_sort, round 2): 11: 0.774 ms,
+                 # 12 (default): 0.660, 13: 0.914 (the 8192-counter zero + scan)
+                 "d11": ["-DLSHB_G2_D=11"],
                  # L1 scatter with 1024-thread CTAs (C4, round 2): E2LSH 0.364 -> 0.353 ms,
                  # SRP LSD passes 1.28 -> 1.34 ms: not kept
                  "s1024": ["-DLSHB_SCATTER_T=1024"],
