@@ -41,6 +41,8 @@ VARIANT_FLAGS = {"b11": ["-DLSHB_G2_IPT=5", "-DLSHB_G2_D=11", "-DLSHB_L1_AVG=512
                  # g2a digit bits below the L1 digit (C4 group_sort, round 2): 11: 0.774 ms,
                  # 12 (default): 0.660, 13: 0.914 (the 8192-counter zero + scan)
                  "d11": ["-DLSHB_G2_D=11"],
+                 # g2a 512 threads x IPT 3 (cap 1536): 3/SM 0.964 ms, 2/SM 1.110 ms at C4 (not kept)
+                 "g512c3": ["-DLSHB_G2_T=512", "-DLSHB_G2_IPT=3", "-DLSHB_G2_CPS=3"],
                  # L1 scatter with 1024-thread CTAs (C4, round 2): E2LSH 0.364 -> 0.353 ms,
                  # SRP LSD passes 1.28 -> 1.34 ms: not kept
                  "s1024": ["-DLSHB_SCATTER_T=1024"],
