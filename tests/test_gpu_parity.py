@@ -618,3 +618,38 @@ def test_group_path_overflow_fallback_and_hint():
         assert (path > 0) == bool(want), (step, path)
         _check_index(idx, lsh.group(keys), p.L)
         idx.close()
+
+
+def test_hcs_register_fed_kernel_equals_tma_kernel(tmp_path):
+    """K2's register-fed slab kernel (used when X cannot be described by a tensor map;
+    forced here with LSH_HCS_NO_TMA=1 in a fresh process — the switch is read once per
+    process) and the TMA-fed default give the same keys bit for bit at full C3 n for both
+    HCS families, and the oracle's on the first 1000 rows."""
+    import subprocess
+    import sys
+    import os
+    c = synth.CONFIGS["C3"]
+    for scheme in ("HCS_E2LSH", "HCS_SRP"):
+        p = _params(c, scheme)
+        h = _handle(p)
+        X = synth.rows(c, 0, c.n, device="cuda")
+        k_tma = h.hash(X, keys=True)["keys"].view(torch.int64).cpu().numpy()
+        out = tmp_path / f"{scheme}.npy"
+        code = (
+            "import sys, numpy as np, torch; sys.path.insert(0, %r)\n"
+            "import paper_2503_06737_b200 as pk, synth\n"
+            "c = synth.CONFIGS['C3']\n"
+            "h = pk.LSH(%r, c.d, c.m, c.L, c.K, c.w, c.hash_seed, mode_d=c.mode_d, mode_m=c.mode_m)\n"
+            "X = synth.rows(c, 0, c.n, device='cuda')\n"
+            "np.save(%r, h.hash(X, keys=True)['keys'].view(torch.int64).cpu().numpy())\n"
+        ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), scheme, str(out))
+        env = dict(os.environ, LSH_HCS_NO_TMA="1")
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        k_reg = np.load(out)
+        assert np.array_equal(k_reg, k_tma), scheme
+        ref = lsh.hash_points(p, lsh.make_tables(p), X[:1000].cpu().numpy())
+        ref["band"] = parity.code_band(p, lsh.make_tables(p), X[:1000].cpu().numpy()) if lsh.is_e2lsh(scheme) \
+            else parity.srp_band(p, lsh.make_tables(p), X[:1000].cpu().numpy())
+        kr = parity.check_keys(p, ref, k_tma[:, :1000].view(np.uint64))
+        assert kr["mismatch_outside_exempt"] == 0, kr
