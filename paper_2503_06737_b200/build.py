@@ -38,6 +38,12 @@ VARIANT_FLAGS = {"b11": ["-DLSHB_G2_IPT=5", "-DLSHB_G2_D=11", "-DLSHB_L1_AVG=512
                  # K1 keys-only loop, tables per unrolled iteration (C4 E2LSH / SRP sketch,
                  # round 2): 1: 0.929 / 0.796 ms, 2 (default): 0.920 / 0.784, 4: 0.929 / 0.776
                  "tu4": ["-DLSHB_SK_TUNROLL=4"],
+                 # K1 keys-only loop with one lane per point and one table per warp iteration
+                 # (the round-2 kernel before the four-tables-per-warp 128-bit gathers)
+                 # (C4, round 2: E2LSH sketch 0.925 lane-per-point -> 0.844 ms four tables per
+                 #  warp; SRP 0.786 -> 0.810 ms, so SRP keeps the lane-per-point loop)
+                 "lane1": ["-DLSHB_SK_QUAD=0"],
+                 "quad2": ["-DLSHB_SK_QUAD=2"],
                  # g2a digit bits below the L1 digit (C4 group_sort, round 2): 11: 0.774 ms,
                  # 12 (default): 0.660, 13: 0.914 (the 8192-counter zero + scan)
                  "d11": ["-DLSHB_G2_D=11"],

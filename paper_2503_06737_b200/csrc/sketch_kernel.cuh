@@ -29,6 +29,11 @@
 #include "discretize.cuh"
 #include "internal.hpp"
 
+#ifndef LSHB_SK_QUAD
+// keys-only path with four tables per warp and 128-bit gathers of four points:
+// 1 = E2LSH keys only (default), 2 = E2LSH and SRP, 0 = never (lane per point)
+#define LSHB_SK_QUAD 1
+#endif
 #ifndef LSHB_SK_TUNROLL
 #define LSHB_SK_TUNROLL 2   // tables per iteration of a warp's keys-only loop
 #endif
@@ -252,6 +257,115 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncthreads();   // the loads above are in flight during the gathers below
         const int64_t row = tile * 32 + lane;
         const bool valid = row < n;
+#if LSHB_SK_QUAD
+        if constexpr (KT > 0 && (E2 || LSHB_SK_QUAD == 2)) {
+            // hot path, four tables per warp: lane = (table j = lane / 8, point quad g =
+            // lane % 8); a lane sums, discretises and keys points 4g..4g+3 of table
+            // 4G + j.  Every gather is ONE 128-bit load of four points' staged word (the
+            // staged row of a coordinate is 32 consecutive points), so a quarter-warp
+            // reads one whole 128-byte row: conflict-free, and a quarter of the
+            // shared-memory instructions and address adds of one gather per point.  The
+            // arithmetic per (bin, point) is the lane-per-point path's, in the same order
+            // (fold, then the pair sum), so the keys are bit-identical.
+            const int j = lane >> 3, g = lane & 7;
+            const char* Tg = reinterpret_cast<const char*>(T) + 16 * g;
+            const int64_t row0 = tile * 32 + 4 * g;
+            for (int G = warp; 4 * G < L; G += kWarps) {
+                const bool tv = 4 * G + j < L;
+                const int t = tv ? 4 * G + j : L - 1;   // a clamped lane computes, never folds or stores
+                {
+                    const uint32_t f1 = tv ? s_fptr[t + 1] : 0u;
+#pragma unroll 1
+                    for (uint32_t f = tv ? s_fptr[t] : 0u; f < f1; ++f) {
+                        const uint32_t e = s_fold[f];
+                        float4* dst = reinterpret_cast<float4*>(const_cast<char*>(Tg) + 4 * (e >> 16));
+                        const float4 b = *reinterpret_cast<const float4*>(Tg + 4 * (e & 0xffffu));
+                        float4 a = *dst;
+                        a.x += b.x;
+                        a.y += b.y;
+                        a.z += b.z;
+                        a.w += b.w;
+                        *dst = a;
+                    }
+                }
+                const uint4* pp4 = reinterpret_cast<const uint4*>(s_pairs + t * KT * 2);
+                uint64_t f[4];
+                if constexpr (E2) {
+                    FpKey fk[4];
+                    float qmax = 0.f;
+                    const float4* co = reinterpret_cast<const float4*>(s_coff + t * KT);
+#pragma unroll
+                    for (int k4 = 0; k4 < KT / 4; ++k4) {
+                        const float4 c4v = co[k4];
+                        const float cc[4] = {c4v.x, c4v.y, c4v.z, c4v.w};
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const uint4 v = pp4[2 * k4 + h];
+                            const float4 a0 = *reinterpret_cast<const float4*>(Tg + v.x);
+                            const float4 a1 = *reinterpret_cast<const float4*>(Tg + v.y);
+                            const float4 b0 = *reinterpret_cast<const float4*>(Tg + v.z);
+                            const float4 b1 = *reinterpret_cast<const float4*>(Tg + v.w);
+                            const float ya[4] = {a0.x + a1.x, a0.y + a1.y, a0.z + a1.z, a0.w + a1.w};
+                            const float yb[4] = {b0.x + b1.x, b0.y + b1.y, b0.z + b1.z, b0.w + b1.w};
+#pragma unroll
+                            for (int p = 0; p < 4; ++p) {
+                                const float qa = fmaf(ya[p], cs, cc[2 * h]);
+                                const float qb = fmaf(yb[p], cs, cc[2 * h + 1]);
+                                qmax = fmax_nan_abs(fmax_nan_abs(qmax, qa), qb);
+                                fk[p].add(__float_as_uint(__fadd_rd(qa, 12582912.0f)));
+                                fk[p].add(__float_as_uint(__fadd_rd(qb, 12582912.0f)));
+                            }
+                        }
+                    }
+                    if (qmax < 4194304.0f) {
+#pragma unroll
+                        for (int p = 0; p < 4; ++p) fk[p].unbias(KT);
+                    } else {
+                        // rare: a code outside the fast floor range (or NaN/Inf) in one of the
+                        // lane's four points: redo all four exactly
+#pragma unroll
+                        for (int p = 0; p < 4; ++p) fk[p] = FpKey();
+#pragma unroll 1
+                        for (int kk = 0; kk < KT; ++kk) {
+                            const uint32_t o1 = s_pairs[2 * (t * KT + kk)], o2 = s_pairs[2 * (t * KT + kk) + 1];
+                            const float c0 = s_coff[t * KT + kk];
+#pragma unroll
+                            for (int p = 0; p < 4; ++p) {
+                                const float y = *reinterpret_cast<const float*>(Tg + o1 + 4 * p) +
+                                                *reinterpret_cast<const float*>(Tg + o2 + 4 * p);
+                                fk[p].add((uint32_t)floor_code(fmaf(y, cs, c0), dz.flags));
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int p = 0; p < 4; ++p) f[p] = fk[p].key();
+                } else {
+                    uint32_t sb[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+                    for (int i = 0; i < KT / 2; ++i) {
+                        const uint4 v = pp4[i];
+                        const float4 a0 = *reinterpret_cast<const float4*>(Tg + v.x);
+                        const float4 a1 = *reinterpret_cast<const float4*>(Tg + v.y);
+                        const float4 b0 = *reinterpret_cast<const float4*>(Tg + v.z);
+                        const float4 b1 = *reinterpret_cast<const float4*>(Tg + v.w);
+                        const float ya[4] = {a0.x + a1.x, a0.y + a1.y, a0.z + a1.z, a0.w + a1.w};
+                        const float yb[4] = {b0.x + b1.x, b0.y + b1.y, b0.z + b1.z, b0.w + b1.w};
+#pragma unroll
+                        for (int p = 0; p < 4; ++p)
+                            sb[p] |= (ya[p] > 0.0f ? 1u : 0u) << (2 * i) | (yb[p] > 0.0f ? 1u : 0u) << (2 * i + 1);
+                    }
+#pragma unroll
+                    for (int p = 0; p < 4; ++p) f[p] = sb[p];
+                }
+                if (tv && out.keys) {
+                    uint64_t* kp = out.keys + (int64_t)t * n + row0;
+#pragma unroll
+                    for (int p = 0; p < 4; ++p)
+                        if (row0 + p < n && LSHB_OK(row0 + p < n)) kp[p] = f[p];
+                }
+            }
+        } else
+#endif
         if constexpr (KT > 0) {
             // hot path: the 3rd, 4th, ... coordinates of a bin are first folded into its
             // first coordinate's staged word (this lane's own column: no other lane or warp
