@@ -44,6 +44,10 @@ VARIANT_FLAGS = {"b11": ["-DLSHB_G2_IPT=5", "-DLSHB_G2_D=11", "-DLSHB_L1_AVG=512
                  #  warp; SRP 0.786 -> 0.810 ms, so SRP keeps the lane-per-point loop)
                  "lane1": ["-DLSHB_SK_QUAD=0"],
                  "quad2": ["-DLSHB_SK_QUAD=2"],
+                 # four-table path with the first 2 / 4 pair-offset vectors read before the fold
+                 # (C4 E2LSH sketch, round 2): 0 (default) 0.848, 2: 0.860, 4: 0.913 ms (spills)
+                 "qpre2": ["-DLSHB_SK_QPRE=2"],
+                 "qpre4": ["-DLSHB_SK_QPRE=4"],
                  # g2a digit bits below the L1 digit (C4 group_sort, round 2): 11: 0.774 ms,
                  # 12 (default): 0.660, 13: 0.914 (the 8192-counter zero + scan)
                  "d11": ["-DLSHB_G2_D=11"],

@@ -34,6 +34,9 @@
 // 1 = E2LSH keys only (default), 2 = E2LSH and SRP, 0 = never (lane per point)
 #define LSHB_SK_QUAD 1
 #endif
+#ifndef LSHB_SK_QPRE
+#define LSHB_SK_QPRE 0      // four-table path: pair-offset vectors read before the fold
+#endif
 #ifndef LSHB_SK_TUNROLL
 #define LSHB_SK_TUNROLL 2   // tables per iteration of a warp's keys-only loop
 #endif
@@ -273,6 +276,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int G = warp; 4 * G < L; G += kWarps) {
                 const bool tv = 4 * G + j < L;
                 const int t = tv ? 4 * G + j : L - 1;   // a clamped lane computes, never folds or stores
+                const uint4* pp4 = reinterpret_cast<const uint4*>(s_pairs + t * KT * 2);
+                // the first pair offsets are read before the fold (their latency overlaps it)
+                constexpr int NPRE = LSHB_SK_QPRE < KT / 2 ? LSHB_SK_QPRE : KT / 2;
+                uint4 pv[NPRE > 0 ? NPRE : 1];
+#pragma unroll
+                for (int i = 0; i < NPRE; ++i) pv[i] = pp4[i];
                 {
                     const uint32_t f1 = tv ? s_fptr[t + 1] : 0u;
 #pragma unroll 1
@@ -288,7 +297,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                         *dst = a;
                     }
                 }
-                const uint4* pp4 = reinterpret_cast<const uint4*>(s_pairs + t * KT * 2);
                 uint64_t f[4];
                 if constexpr (E2) {
                     FpKey fk[4];
@@ -300,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const float cc[4] = {c4v.x, c4v.y, c4v.z, c4v.w};
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
-                            const uint4 v = pp4[2 * k4 + h];
+                            const uint4 v = 2 * k4 + h < NPRE ? pv[(2 * k4 + h) % (NPRE > 0 ? NPRE : 1)] : pp4[2 * k4 + h];
                             const float4 a0 = *reinterpret_cast<const float4*>(Tg + v.x);
                             const float4 a1 = *reinterpret_cast<const float4*>(Tg + v.y);
                             const float4 b0 = *reinterpret_cast<const float4*>(Tg + v.z);
@@ -343,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint32_t sb[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
                     for (int i = 0; i < KT / 2; ++i) {
-                        const uint4 v = pp4[i];
+                        const uint4 v = i < NPRE ? pv[i % (NPRE > 0 ? NPRE : 1)] : pp4[i];
                         const float4 a0 = *reinterpret_cast<const float4*>(Tg + v.x);
                         const float4 a1 = *reinterpret_cast<const float4*>(Tg + v.y);
                         const float4 b0 = *reinterpret_cast<const float4*>(Tg + v.z);
