@@ -204,3 +204,31 @@ def test_c5_keys_only_sampled(scheme, parity_log):
     ref = _oracle(p, Xs)
     _check(p, ref, gk[:, rows], "C5/keys_only_sampled", parity_log)
 
+
+
+@pytest.mark.parametrize("K,L,d,m", [(8, 5, 64, 40), (16, 3, 200, 48)])
+def test_fast_path_large_codes_and_partial_table_groups(K, L, d, m, parity_log):
+    """The E2LSH keys-only kernel takes four tables per warp (L % 4 != 0 here: clamped
+    lanes compute but never fold or store) and four points per lane; a code outside
+    the fast floor's range (|q| >= 2^22, here rows scaled by 10^5 among unscaled rows,
+    ragged n) sends the lane's four points through the exact floor.  Keys equal the
+    generic instantiation bit for bit and the oracle outside the exemption bands
+    (Def. CS-E2LSH; reading B9, floor toward -inf)."""
+    p = lsh.Params("CS_E2LSH", d=d, m=m, L=L, K=K, w=0.05, seed=11)
+    h = _handle(p)
+    X = synth.gaussian_rows_like(203, d, 17, device="cuda")
+    X[3] *= 1e5
+    X[41] *= 1e5
+    X[200] *= -1e5
+    k_fast = h.hash(X, keys=True)["keys"]
+    out = h.hash(X, keys=True, codes=True)
+    torch.cuda.synchronize()
+    h.check()
+    assert torch.equal(k_fast.view(torch.int64), out["keys"].view(torch.int64))
+    codes = out["codes"].cpu().numpy()
+    assert np.abs(codes).max() >= 4194304   # the exact-floor branch was taken
+    ref = _oracle(p, X.cpu().numpy())
+    kr = parity.check_keys(p, ref, _u64(k_fast))
+    parity_log({"test": f"large_codes/K{K}_L{L}", "scheme": p.scheme, "keys": kr["n"],
+                "key_mismatch_outside_exempt": kr["mismatch_outside_exempt"], "exempt_keys": kr["exempt"]})
+    assert kr["mismatch_outside_exempt"] == 0, kr
