@@ -23,6 +23,7 @@ done
 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $F/prof/bench_short.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $F/prof/bench_launches.csv \
     python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $F/prof/ncu_launch.log 2>&1
+python tools/launch_shares.py $F/prof/bench_launches.csv > $F/prof/launch_shares.txt 2>&1
 timeout 900 python bench.py > $F/legs/C4_CS_E2LSH.log 2>&1
 for W in "--scheme CS_SRP" "--config C5 --scheme HCS_E2LSH --steps 3" "--config C5 --scheme HCS_SRP --steps 3" \
          "--config C3 --scheme HCS_E2LSH" "--config C3 --scheme HCS_SRP" "--config C2 --scheme CS_E2LSH" "--config C2 --scheme CS_SRP" \
