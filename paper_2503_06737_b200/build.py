@@ -44,6 +44,9 @@ VARIANT_FLAGS = {"b11": ["-DLSHB_G2_IPT=5", "-DLSHB_G2_D=11", "-DLSHB_L1_AVG=512
                  #  warp; SRP 0.786 -> 0.810 ms, so SRP keeps the lane-per-point loop)
                  "lane1": ["-DLSHB_SK_QUAD=0"],
                  "quad2": ["-DLSHB_SK_QUAD=2"],
+                 # (also measured, source reverted: the thread index pinned in a register so the
+                 #  tile loop has no S2R after its barriers — C4 E2LSH sketch 0.849 vs 0.847 ms,
+                 #  SRP 0.787 vs 0.787: the samples at those S2R were warps waiting at the barrier)
                  # four-table path with the first 2 / 4 pair-offset vectors read before the fold
                  # (C4 E2LSH sketch, round 2): 0 (default) 0.848, 2: 0.860, 4: 0.913 ms (spills)
                  "qpre2": ["-DLSHB_SK_QPRE=2"],
