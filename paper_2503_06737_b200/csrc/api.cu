@@ -1014,7 +1014,7 @@ extern "C" lsh_status lsh_query_buckets(const lsh_handle* h, const lsh_index* id
     if (st == LSH_OK) {
         CK(index_acquire(idx, s));
         timing_begin("lookup", s);
-        cudaError_t e = launch_lookup(qk, nq, h->p.L, idx->n, idx->dev, begin, end, s);
+        cudaError_t e = launch_lookup(qk, nq, h->p.L, idx->n, idx->dev, begin, end, h->key_width == 64, s);
         count_launch();
         timing_end("lookup", s);
         if (e != cudaSuccess) st = cuda_fail(e, "lookup");

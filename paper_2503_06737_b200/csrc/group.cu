@@ -1763,8 +1763,15 @@ cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_bas
 // K5: bucket lookup of query keys ("collect the index of all the
 // elements ... hashed in hbar_t(q)").
 // ---------------------------------------------------------------------------
+// interp (64-bit fingerprint keys, uniform over [0, 2^64)): up to three rounds that
+// interpolate the key's position between the current bounds and probe two positions
+// a few standard deviations around it (independent loads: one memory round trip per
+// round), then the binary search finishes.  Every probe only moves lo or hi past an
+// index whose key is known to be < or >= the query key, so the result is the
+// lower bound in every case (equal to the plain binary search), only the number of
+// dependent loads changes (~9 instead of ~20 at 10^6 buckets).
 __global__ void lookup_kernel(const uint64_t* __restrict__ qkeys, int64_t nq, int L, int64_t n, IndexDev idx,
-                              int64_t* __restrict__ begin, int64_t* __restrict__ end) {
+                              int64_t* __restrict__ begin, int64_t* __restrict__ end, int interp) {
     const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (gi >= nq * L) return;
     const int64_t q = gi / L;
@@ -1772,14 +1779,43 @@ __global__ void lookup_kernel(const uint64_t* __restrict__ qkeys, int64_t nq, in
     const uint64_t key = qkeys[(int64_t)t * nq + q];
     const uint64_t* uk = idx.ukeys + (int64_t)t * n;
     const uint32_t* of = idx.offs + (int64_t)t * (n + 1);
-    int64_t lo = 0, hi = idx.nb[t];
+    const int64_t nb = idx.nb[t];
+    // invariant: uk[i] < key for i < lo, uk[i] >= key for i >= hi; the keys in [lo, hi)
+    // lie in [klo, khi]
+    int64_t lo = 0, hi = nb;
+    uint64_t klo = 0, khi = ~0ull;
+    if (interp) {
+#pragma unroll 1
+        for (int r = 0; r < 3 && hi - lo > 64; ++r) {
+            const double span = (double)(hi - lo);
+            double phi = key <= klo ? 0.0 : key >= khi ? 1.0 : (double)(key - klo) / (double)(khi - klo);
+            const int64_t g = lo + (int64_t)(phi * span);
+            const int64_t dl = 2 + (int64_t)(2.0 * sqrt(span));
+            const int64_t p1 = max(lo, g - dl), p2 = min(hi - 1, g + dl);
+            const uint64_t v1 = uk[p1], v2 = uk[p2];
+            if (v1 >= key) {
+                hi = p1;
+                khi = v1;
+            } else {
+                lo = p1 + 1;
+                klo = v1;
+                if (v2 >= key) {
+                    hi = p2;
+                    khi = v2;
+                } else {
+                    lo = p2 + 1;
+                    klo = v2;
+                }
+            }
+        }
+    }
     while (lo < hi) {
         const int64_t mid = (lo + hi) >> 1;
         if (uk[mid] < key) lo = mid + 1;
         else hi = mid;
     }
     int64_t b, e;
-    if (lo < idx.nb[t] && uk[lo] == key) {
+    if (lo < nb && uk[lo] == key) {
         b = of[lo];
         e = of[lo + 1];
     } else {
@@ -1790,10 +1826,10 @@ __global__ void lookup_kernel(const uint64_t* __restrict__ qkeys, int64_t nq, in
 }
 
 cudaError_t launch_lookup(const uint64_t* qkeys, int64_t nq, int L, int64_t n, const IndexDev& idx, int64_t* begin,
-                          int64_t* end, cudaStream_t s) {
+                          int64_t* end, bool interp, cudaStream_t s) {
     if (nq == 0) return cudaSuccess;
     const int64_t tot = nq * L;
-    lookup_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(qkeys, nq, L, n, idx, begin, end);
+    lookup_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(qkeys, nq, L, n, idx, begin, end, interp ? 1 : 0);
     return cudaGetLastError();
 }
 

@@ -156,8 +156,9 @@ size_t group_key_slots(int64_t n, int key_width);   // per-table L1 output slots
 bool group_is_lsd(int key_width);
 cudaError_t launch_group(const uint64_t* keys, int64_t n, int L, uint32_t id_base, int key_width,
                          GroupScratch& sc, IndexDev& out, int* flags, cudaStream_t s);
+// interp: keys are 64-bit fingerprints (uniform): interpolation-guided probes first
 cudaError_t launch_lookup(const uint64_t* qkeys, int64_t nq, int L, int64_t n, const IndexDev& idx,
-                          int64_t* begin, int64_t* end, cudaStream_t s);
+                          int64_t* begin, int64_t* end, bool interp, cudaStream_t s);
 cudaError_t launch_knn(const IndexDev& idx, int64_t n, int L, uint32_t id_base, const int64_t* begin,
                        const int64_t* end, const float* X, int64_t ldx, int d, const float* Q, int64_t ldq,
                        int64_t nq, int k, int max_cand, int cosine, int64_t* out_ids, float* out_score,

@@ -232,3 +232,35 @@ def test_fast_path_large_codes_and_partial_table_groups(K, L, d, m, parity_log):
     parity_log({"test": f"large_codes/K{K}_L{L}", "scheme": p.scheme, "keys": kr["n"],
                 "key_mismatch_outside_exempt": kr["mismatch_outside_exempt"], "exempt_keys": kr["exempt"]})
     assert kr["mismatch_outside_exempt"] == 0, kr
+
+
+@pytest.mark.parametrize("scheme", ["CS_E2LSH", "CS_SRP"])
+def test_c4_query_buckets(scheme):
+    """Query lookup at the bench's scale (10^6 buckets per E2LSH table, where the
+    interpolation-guided probes run before the binary search): (begin, end) of 1000
+    indexed points and 1000 fresh points in every table equal the lower-bound lookup of
+    their keys in the built tables (the bucket hbar_t(q)); indexed points
+    find themselves."""
+    c = synth.CONFIGS["C4"]
+    p = _params(c, scheme)
+    h = _handle(p)
+    X = synth.rows(c, 0, c.n, device="cuda")
+    idx = h.build_index(X, id_base=0)
+    Q = torch.cat([X[:1000], synth.gaussian_rows_like(1000, c.d, 91, device="cuda")])
+    b, e = h.query_buckets(idx, Q)
+    qk = _u64(h.hash(Q, keys=True)["keys"])
+    torch.cuda.synchronize()
+    b, e = b.cpu().numpy(), e.cpu().numpy()
+    for t in range(p.L):
+        ids, uk, of = (x.cpu().numpy() for x in idx.view(t))
+        uk = uk.astype(np.uint64)
+        of = of.astype(np.int64)
+        pos = np.searchsorted(uk, qk[t], side="left")
+        hit = (pos < uk.shape[0]) & (uk[np.minimum(pos, uk.shape[0] - 1)] == qk[t])
+        eb = of[pos]
+        ee = np.where(hit, of[np.minimum(pos + 1, of.shape[0] - 1)], eb)
+        assert np.array_equal(b[:, t], eb), t
+        assert np.array_equal(e[:, t], ee), t
+        for q in range(0, 1000, 37):
+            assert q in ids[b[q, t]:e[q, t]].tolist(), (t, q)
+    idx.close()
