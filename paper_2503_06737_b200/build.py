@@ -43,7 +43,7 @@ VARIANT_FLAGS = {"b11": ["-DLSHB_G2_IPT=5", "-DLSHB_G2_D=11", "-DLSHB_L1_AVG=512
                  # (C4, round 2: E2LSH sketch 0.925 lane-per-point -> 0.844 ms four tables per
                  #  warp; SRP 0.786 -> 0.810 ms, so SRP keeps the lane-per-point loop)
                  "lane1": ["-DLSHB_SK_QUAD=0"],
-                 "quad2": ["-DLSHB_SK_QUAD=2"],
+                 "quad1": ["-DLSHB_SK_QUAD=1"],
                  # (also measured, source reverted: the thread index pinned in a register so the
                  #  tile loop has no S2R after its barriers — C4 E2LSH sketch 0.849 vs 0.847 ms,
                  #  SRP 0.787 vs 0.787: the samples at those S2R were warps waiting at the barrier)
@@ -59,6 +59,19 @@ VARIANT_FLAGS = {"b11": ["-DLSHB_G2_IPT=5", "-DLSHB_G2_D=11", "-DLSHB_L1_AVG=512
                  # L1 scatter with 1024-thread CTAs (C4, round 2): E2LSH 0.364 -> 0.353 ms,
                  # SRP LSD passes 1.28 -> 1.34 ms: not kept
                  "s1024": ["-DLSHB_SCATTER_T=1024"],
+                 # K1 four-table path key stores and streamed-load L2 hints (C4 E2LSH / SRP sketch,
+                 # end of round 2).  A lane's four keys as four 64-bit stores (32-byte lane stride:
+                 # every store instruction touched all 32 sectors of the warp's 1 KB): 0.846 ms;
+                 # two 128-bit stores: 0.784; ONE 256-bit store (the default): 0.771.  With it the
+                 # four-table loop also wins for SRP (0.788 lane-per-point -> 0.712), so it is the
+                 # default for both families.  X loads: L2::256B prefetch size 0.847 (no change);
+                 # an L2 evict_first policy 0.846 -> 0.837 (E2LSH), 0.787 -> 0.793 (SRP lane-per-point).
+                 "k1old": ["-DLSHB_SK_QUAD=1", "-DLSHB_SK_ST128=0"],
+                 "st128": ["-DLSHB_SK_ST128=1"],
+                 "st256cs": ["-DLSHB_SK_ST128=3"],
+                 "ld256": ["-DLSHB_SK_LDHINT=1"],
+                 "ef": ["-DLSHB_SK_LDHINT=2"],
+                 "efe2": ["-DLSHB_SK_LDHINT=4"],
                  "b9": ["-DLSHB_L1_AVG=2048", "-DLSHB_G2_T=256", "-DLSHB_G2_IPT=10", "-DLSHB_G2_CPS=3", "-DLSHB_G2_D=13"]}
 
 def nvcc() -> str:

@@ -31,8 +31,8 @@
 
 #ifndef LSHB_SK_QUAD
 // keys-only path with four tables per warp and 128-bit gathers of four points:
-// 1 = E2LSH keys only (default), 2 = E2LSH and SRP, 0 = never (lane per point)
-#define LSHB_SK_QUAD 1
+// 1 = E2LSH keys only, 2 = E2LSH and SRP (default), 0 = never (lane per point)
+#define LSHB_SK_QUAD 2
 #endif
 #ifndef LSHB_SK_QPRE
 #define LSHB_SK_QPRE 0      // four-table path: pair-offset vectors read before the fold
@@ -49,11 +49,35 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kTUnroll = LSHB_SK_TUNROLL;
 constexpr int CW = kSketchColWords;   // words per staged float4 column (4 coordinates x 32 points + pad)
 
+#ifndef LSHB_SK_LDHINT
+// streamed X loads: 0 plain, 1 L2::256B prefetch size, 2 L2::evict_first policy, 3 both,
+// 4 evict_first in the E2LSH instantiations only
+#define LSHB_SK_LDHINT 0
+#endif
+#ifndef LSHB_SK_ST128
+// four-table path, a lane's four keys: 0 four 64-bit stores, 1 two 128-bit stores, 2 one
+// 256-bit store (3: with .cs) when the address is aligned, else the narrower forms
+#define LSHB_SK_ST128 2
+#endif
+#if LSHB_SK_LDHINT == 1 || LSHB_SK_LDHINT == 3
+#define LSHB_SK_LDQ ".L2::256B"
+#else
+#define LSHB_SK_LDQ ""
+#endif
+template <bool EF>
 __device__ __forceinline__ float4 ldg_stream_f4(const float* p) {
     float4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-                 : "l"(p));
+    if constexpr (EF) {
+        uint64_t pol;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint" LSHB_SK_LDQ ".v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                     : "l"(p), "l"(pol));
+    } else {
+        asm volatile("ld.global.nc.L1::no_allocate" LSHB_SK_LDQ ".v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                     : "l"(p));
+    }
     return r;
 }
 __device__ __forceinline__ float ldg_stream_f1(const float* p) {
@@ -170,6 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     float4 buf[VEC ? RG * 4 : VS];
 
     // row groups [i0, i1) of the thread's column (VEC); the scalar path ignores them
+    constexpr bool kEF = LSHB_SK_LDHINT == 2 || LSHB_SK_LDHINT == 3 || (LSHB_SK_LDHINT == 4 && E2);
     auto load = [&](int64_t tl, int i0 = 0, int i1 = 1 << 20) {
         if constexpr (VEC) {
             if (col_ok) {
@@ -180,11 +205,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const float* src = X + r * ld + 4 * c;
                     if (tl * 32 + 32 <= n) {
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) buf[4 * i + j] = ldg_stream_f4(src + j * ld);
+                        for (int j = 0; j < 4; ++j) buf[4 * i + j] = ldg_stream_f4<kEF>(src + j * ld);
                     } else {
 #pragma unroll
                         for (int j = 0; j < 4; ++j)
-                            buf[4 * i + j] = r + j < n ? ldg_stream_f4(src + j * ld) : make_float4(0.f, 0.f, 0.f, 0.f);
+                            buf[4 * i + j] = r + j < n ? ldg_stream_f4<kEF>(src + j * ld) : make_float4(0.f, 0.f, 0.f, 0.f);
                     }
                 }
             }
@@ -367,6 +392,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 if (tv && out.keys) {
                     uint64_t* kp = out.keys + (int64_t)t * n + row0;
+#if LSHB_SK_ST128 >= 2
+                    if (row0 + 4 <= n && (reinterpret_cast<uintptr_t>(kp) & 31) == 0) {
+#if LSHB_SK_ST128 == 3
+                        asm volatile("st.global.cs.v4.b64 [%0], {%1,%2,%3,%4};" ::"l"(kp), "l"(f[0]), "l"(f[1]), "l"(f[2]),
+                                     "l"(f[3])
+                                     : "memory");
+#else
+                        asm volatile("st.global.v4.b64 [%0], {%1,%2,%3,%4};" ::"l"(kp), "l"(f[0]), "l"(f[1]), "l"(f[2]),
+                                     "l"(f[3])
+                                     : "memory");
+#endif
+                    } else
+#endif
+#if LSHB_SK_ST128
+                    if (row0 + 4 <= n && (reinterpret_cast<uintptr_t>(kp) & 15) == 0) {
+                        reinterpret_cast<ulonglong2*>(kp)[0] = make_ulonglong2(f[0], f[1]);
+                        reinterpret_cast<ulonglong2*>(kp)[1] = make_ulonglong2(f[2], f[3]);
+                    } else
+#endif
 #pragma unroll
                     for (int p = 0; p < 4; ++p)
                         if (row0 + p < n && LSHB_OK(row0 + p < n)) kp[p] = f[p];
