@@ -234,6 +234,33 @@ def test_fast_path_large_codes_and_partial_table_groups(K, L, d, m, parity_log):
     assert kr["mismatch_outside_exempt"] == 0, kr
 
 
+@pytest.mark.parametrize("n", [200, 202, 203, 5])
+@pytest.mark.parametrize("scheme,K,L,d,m", [("CS_E2LSH", 16, 6, 200, 96), ("CS_SRP", 16, 7, 200, 112),
+                                            ("CS_E2LSH", 8, 5, 64, 40), ("CS_SRP", 8, 9, 64, 72)])
+def test_four_table_key_store_forms(scheme, K, L, d, m, n, parity_log):
+    """The four-table keys-only loop (both families) writes a lane's four keys with one
+    256-bit store when (t n + row) * 8 is 32-byte aligned, else two 128-bit stores, else
+    four 64-bit stores: n = 200 takes the 256-bit form in every table, n = 202 alternates
+    256- / 128-bit by table parity, n = 203 mixes all three and has a ragged last quad,
+    n = 5 is a single partial tile.  Keys equal the generic instantiation bit for bit and
+    the oracle outside the exemption bands (PAPER.md:314 Def. CS-E2LSH, :918 Def. CS-SRP;
+    :155 the table keys)."""
+    p = lsh.Params(scheme, d=d, m=m, L=L, K=K, w=0.7, seed=23)
+    h = _handle(p)
+    X = synth.gaussian_rows_like(n, d, 29, device="cuda")
+    k_fast = h.hash(X, keys=True)["keys"]
+    dbg = dict(codes=True) if lsh.is_e2lsh(scheme) else dict(bits=True)
+    k_gen = h.hash(X, keys=True, **dbg)["keys"]
+    torch.cuda.synchronize()
+    h.check()
+    assert torch.equal(k_fast.view(torch.int64), k_gen.view(torch.int64))
+    ref = _oracle(p, X.cpu().numpy())
+    kr = parity.check_keys(p, ref, _u64(k_fast))
+    parity_log({"test": f"store_forms/{scheme}_K{K}_n{n}", "scheme": p.scheme, "keys": kr["n"],
+                "key_mismatch_outside_exempt": kr["mismatch_outside_exempt"], "exempt_keys": kr["exempt"]})
+    assert kr["mismatch_outside_exempt"] == 0, kr
+
+
 @pytest.mark.parametrize("scheme", ["CS_E2LSH", "CS_SRP"])
 def test_c4_query_buckets(scheme):
     """Query lookup at the bench's scale (10^6 buckets per E2LSH table, where the
